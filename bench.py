@@ -1,0 +1,346 @@
+"""Benchmark: seconds per Gauss-Newton registration (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 256]
+
+Workload (N=1): C2 of SURVEY.md §8(d) -- sphere -> deformed sphere, 256^3,
+cubic, n_t=4, beta_v=1e-2, beta_w=0, GN-PCG to gtol 5e-2; one step = one full
+`gauss_newton_register` with m0/m1 resident in HBM (value), and one full
+`register()` call from pinned host buffers incl. label transport + Dice and
+the velocity/deformed-image read-back (e2e).  Synthetic data.
+
+N > 1 (this round): independent replicas of the same registration on every
+rank ("weak", no data-path collective yet), max-over-ranks device time.
+
+--impl reference: the CPU oracle (oracle/velreg_oracle.py, numpy + numba, all
+host threads) on a bounded sample of the same workload (one objective
+evaluation, reduced gradient, Gauss-Newton matvec and preconditioner apply at
+256^3), extrapolated to one registration with C2's operation counts.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+# C2 operation counts of the reference trajectory (tests/golden/c2_256.json):
+# 4 GN iterations, 1 Armijo trial each, PCG 1/1/4/11.
+C2_COUNTS = {"objective": 5, "gradient": 5, "matvec": 17, "precond": 21}
+METRIC = "sec per GN registration @256^3 (C2 sphere->deformed sphere, cubic, n_t=4)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------
+# CPU reference arm (oracle port timed on the host cores)
+# ----------------------------------------------------------------------------
+def cpu_sample(n: int) -> dict:
+    """Time one of each operation class of a C2 registration at n^3 on the CPU
+    oracle and extrapolate to one registration with C2's counts."""
+    import numpy as np
+    from oracle import velreg_oracle as O
+    import numba
+
+    dims = (n, n, n)
+    x = O.lattice(dims)
+    r = np.sqrt(sum((x[i] - math.pi) ** 2 for i in range(3)))
+    m0 = (0.5 * (1.0 - np.tanh((r - 1.2) / 0.19635))).astype(np.float32)
+    vtrue = 0.2 * O.velocity(2, dims)
+    m1 = O.Transport(vtrue, 4, "cubic").state_series(m0)[-1]
+    v = 0.5 * vtrue
+    t = {}
+    t0 = time.perf_counter()
+    pb = O.Problem(m0, m1, v, beta_v=1e-2, beta_w=0.0, n_t=4, order="cubic")
+    pb.objective()
+    t["objective"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g = pb.gradient()
+    t["gradient"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pb.matvec(g)
+    t["matvec"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.op_inv_shifted(g, 1e-2, 1.0)
+    t["precond"] = time.perf_counter() - t0
+    total = sum(C2_COUNTS[k] * t[k] for k in C2_COUNTS)
+    return {"value": total, "unit": "s", "cores": numba.get_num_threads(), "kind": "port",
+            "sample": (f"oracle at {n}^3: 1 objective ({t['objective']:.2f}s) + 1 gradient ({t['gradient']:.2f}s)"
+                       f" + 1 GN matvec ({t['matvec']:.2f}s) + 1 precond ({t['precond']:.2f}s), extrapolated x"
+                       f" C2 counts {C2_COUNTS}"),
+            "sample_seconds": sum(t.values()), "parts": t}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import velreg_oracle as O
+    import numpy as np
+    # JIT warm-up (tiny grid) counts as warm-up work
+    for _ in range(max(1, min(args.warmup, 1))):
+        O.gauss_newton(*(np.random.default_rng(0).random((2, 16, 16, 16)).astype(np.float32)), max_gn=1)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(args.n)
+        vals.append(last["value"])
+    val = sorted(vals)[len(vals) // 2]
+    line = {"metric": METRIC, "value": val, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 sphere->deformed sphere {args.n}^3, cubic, n_t=4, beta_v=1e-2, beta_w=0",
+                       "cpu": "oracle port (numpy pocketfft single-thread + numba parallel gathers)"},
+            "impl": "reference",
+            "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms in the background."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2209_08189_b200 as P
+    from paper_2209_08189_b200 import _lib
+    from paper_2209_08189_b200.synth import c2_problem
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = args.n
+    g = P.make_grid((n, n, n))
+    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=0.0, n_t=4, interp_order="cubic")
+    m0, m1, l0, l1, _ = c2_problem(g)
+    l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    def one():
+        return P.gauss_newton_register(m0, m1, cfg)
+
+    for _ in range(args.warmup):
+        v, diag = one()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs ---------------------------------
+    stream = torch.cuda.current_stream()
+    dominant = "vr_advect"
+    _lib.PROFILE.reset(timed=(dominant, "vr_spec_apply", "vr_trace_rk2", "vr_fd8_grad"))
+    clocks = ClockSampler(local)
+    times = []
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for _ in range(args.steps):
+        flush_l2(l2_flush)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        _lib.PROFILE.enabled = True
+        a.record(stream)
+        v, diag = one()
+        b.record(stream)
+        _lib.PROFILE.enabled = False
+        b.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = _lib.PROFILE.total_launches()
+    kern = {name: _lib.PROFILE.avg_ms(name) for name in _lib.PROFILE.timed}
+    t_step = max_over_ranks(sum(times) / len(times))
+    value = t_step / ws   # whole-job seconds per registration (replicas)
+
+    # ---- e2e through the public API from pinned host buffers -------------------
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+    h_m0 = torch.from_numpy(m0.numpy()).pin_memory()
+    h_m1 = torch.from_numpy(m1.numpy()).pin_memory()
+    h_l0 = torch.from_numpy(l0.numpy()).pin_memory()
+    h_l1 = torch.from_numpy(l1.numpy()).pin_memory()
+    h_v = torch.empty((3, n, n, n), dtype=torch.float32).pin_memory()
+    h_def = torch.empty((n, n, n), dtype=torch.float32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in (h_m0, h_m1, h_l0, h_l1))
+    d2h = h_v.numel() * 4 + h_def.numel() * 4 + 8
+    e2e_times = []
+    dice = None
+    for _ in range(e2e_steps):
+        flush_l2(l2_flush)
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        d_m0 = h_m0.to("cuda", non_blocking=True)
+        d_m1 = h_m1.to("cuda", non_blocking=True)
+        d_l0 = h_l0.to("cuda", non_blocking=True)
+        d_l1 = h_l1.to("cuda", non_blocking=True)
+        res = P.register(P.ScalarField(g, d_m0), P.ScalarField(g, d_m1), cfg, labels0=d_l0, labels1=d_l1)
+        h_v.copy_(res.velocity.data, non_blocking=True)
+        h_def.copy_(res.deformed.values, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        dice = res.dice.d_a
+        e2e_times.append(a.elapsed_time(b) / 1e3)
+    e2e_val = max_over_ranks(sum(e2e_times) / len(e2e_times)) / ws
+
+    # ---- roofline of the dominant kernel -------------------------------------
+    peaks = measured_peaks()
+    per_unit = 20.0  # B per interpolated point: 12 B characteristic + 4 B out + 4 B source
+    avg_ms, nlaunch = kern.get(dominant, (0.0, 0))
+    achieved = (per_unit * g.num_voxels / (avg_ms * 1e-3) / 1e9) if avg_ms > 0 else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as fh:
+            traffic = json.load(fh).get(dominant)
+    step_ms = t_step * 1e3
+    kernels = {k: {"avg_ms": round(v[0], 5), "launches_per_step": v[1] // max(args.steps, 1),
+                   "share_of_step": round(v[0] * v[1] / max(args.steps, 1) / step_ms, 4)}
+               for k, v in kern.items()}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cb = cpu_sample(n)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (f64 reductions / forward spectra)", "data": "synthetic",
+            "config": {"workload": f"C2 sphere->deformed sphere {n}^3 GN-PCG, cubic, n_t=4, beta_v=1e-2, "
+                                   f"beta_w=0, gtol=5e-2", "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "256 MB buffer written between timed steps; working set > 126 MB L2",
+                       "gn_iterations": diag.gn_iterations,
+                       "pcg": [r.pcg_iterations for r in diag.iterations],
+                       "matvecs": diag.matvecs, "relative_residual": diag.relative_residual,
+                       "launches_per_step": launches // max(args.steps, 1),
+                       "dice_post": dice},
+            "e2e": {"value": e2e_val, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "advect_kernel<cubic> (vr_advect)",
+                         "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
+                         "peak_source": peaks["source"], "bytes_per_unit": per_unit,
+                         "units_per_launch": g.num_voxels, "avg_launch_ms": avg_ms},
+            "kernels": kernels,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * libvelreg_b200 -- C ABI of the B200-native (sm_100a) registration hot path.
+ *
+ * Drop-in boundary for the stationary-velocity Gauss-Newton-Krylov path of the
+ * reference package `velreg` (/root/reference/pkg/src/velreg).  The reference
+ * has no FFI layer: its operators are Python functions over numpy arrays and
+ * its only native code is the numba kernel call
+ *     kern(vals, px, py, pz, out, h1, h2, h3)          (interp.py:127)
+ * Every entry below replaces one of those Python operators; the Python host
+ * package (paper_2209_08189_b200/) keeps the reference's names, argument
+ * meaning and exception classes on top of it.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; the caller owns them.
+ *  - dims = {N1, N2, N3}, C order, x3 contiguous (grid.py:3-5); vector fields
+ *    are SoA float[3][N1][N2][N3] (grid.py:99).  One field must have < 2^31
+ *    voxels.
+ *  - Characteristics are displacements in index units: the departure point of
+ *    voxel (i,j,k) is (i-d1, j-d2, k-d3).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All calls are
+ *    asynchronous; reductions write f64 results to device memory.
+ *  - Return 0 on success, negative VR_ERR_* on invalid arguments / launch
+ *    failure.  Non-finite results are reported through an optional device int
+ *    flag (set to non-zero), read back where the reference checks
+ *    (transport.py:57-59,119-121; optim.py:157-158,179-180).
+ */
+#ifndef VELREG_B200_H
+#define VELREG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VR_ORDER_LINEAR 1
+#define VR_ORDER_CUBIC 3
+
+/* spectral operator kinds (diffops.py:108-154) */
+#define VR_SPEC_IDENTITY 0  /* FFT round trip (SpectralWorkspace.forward/inverse, diffops.py:51-55) */
+#define VR_SPEC_A 1         /* apply_A, symbol |k|^2 (diffops.py:116-118) */
+#define VR_SPEC_INVSHIFT 2  /* apply_inv_shifted_A, 1/(beta_v|k|^2+shift) (diffops.py:121-126) */
+#define VR_SPEC_K 3         /* apply_K Leray blend (diffops.py:129-146) */
+#define VR_SPEC_GAUSS 4     /* Gaussian smoothing exp(-sigma^2|k|^2/2) (north-star extra, no ref) */
+#define VR_SPEC_A2 5        /* H2 operator |k|^4 (north-star extra, no ref) */
+#define VR_SPEC_INVSHIFT2 6 /* 1/(beta_v|k|^4+shift) (north-star extra, no ref) */
+
+#define VR_RED_SUM 0
+#define VR_RED_MINMAX 1
+
+typedef struct vr_spec_plan vr_spec_plan;
+
+/* ---- interpolation (interp.py:112-128 interpolate_values) ------------------
+ * out[p] = periodic trilinear (order 1) / tricubic-Lagrange (order 3)
+ * interpolant of src at points pts[0..2][p] given in RADIANS (any finite
+ * value; wrapped).  pts is float32 (pts_is_f64 = 0) or float64 (1). */
+int vr_interp_points(const float* src, const int64_t dims[3], const void* pts, int pts_is_f64, int64_t npts,
+                     int order, float* out, void* stream);
+
+/* ---- characteristics (transport.py:66-76 trace_characteristics and
+ * transport.py:94-110 TransportOperators.__init__) ----------------------------
+ * Forward and backward RK2 traces of velocity v (3 x N, rad / unit time).
+ * If div != NULL also the trapezoidal source factors
+ *   fac_jac = jac_numer/jac_denom, fac_adj = adj_numer/adj_denom. */
+int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, float* disp_fwd, float* disp_bwd,
+                 const float* div, float* fac_jac, float* fac_adj, void* stream);
+
+/* displacement -> absolute points wrapped to [0, 2pi) (Characteristics.points) */
+int vr_disp_to_points(const float* disp, const int64_t dims[3], double* pts, void* stream);
+
+/* ---- semi-Lagrangian sweeps -------------------------------------------------
+ * one step dst = interp(src, X) [* factor]:
+ *   state    transport.py:130-133 (factor NULL, forward trace)
+ *   adjoint  transport.py:154-155 (factor = fac_adj, backward trace)
+ *   Jacobian transport.py:194-195 (factor = fac_jac, forward trace) */
+int vr_advect(const float* src, const int64_t dims[3], const float* disp, const float* factor, int order,
+              float* dst, int* nonfinite_flag, void* stream);
+
+/* incremental state (transport.py:160-185): u0 = dt/2 * s_0, s_j = -vt.grad m^j */
+int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3], double dt, float* u0,
+                     void* stream);
+/* m~_{j+1} = interp(u_j) + dt/2 s_{j+1}; writes u_{j+1} = m~_{j+1} + dt/2 s_{j+1}
+ * (last = 0), m~_n itself (last = 1) or -m~_n, the incremental adjoint's final
+ * condition (optim.py:206), (last = 2) */
+int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fwd, const float* vt,
+                     const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
+                     void* stream);
+
+/* trapezoidal body force sum_j w_j lam^j grad m^j (optim.py:162-171);
+ * lam_series (n_t+1) x N, gradm_series (n_t+1) x 3 x N */
+int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
+                  float* out, void* stream);
+
+/* label transport step (synth.py:121-131): source = labels_in==label_id
+ * (if labels_in) else src; destination = float field (dst) or thresholded
+ * write of label_id where value >= 0.5 (labels_out). */
+int vr_label_step(const float* src, const int* labels_in, int label_id, const int64_t dims[3], const float* disp,
+                  int order, float* dst, int* labels_out, void* stream);
+
+/* ---- FD8 (diffops.py:84-105); bit-identical to numpy for float32 input ---- */
+int vr_fd8_grad(const float* f, const int64_t dims[3], float* out3, void* stream);
+int vr_fd8_div(const float* v3, const int64_t dims[3], float* out, void* stream);
+
+/* ---- spectral (diffops.py:24-55 SpectralWorkspace; :108-154 operators) ---- */
+int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** plan);
+int vr_spec_plan_destroy(vr_spec_plan* plan);
+int vr_spec_plan_dims(const vr_spec_plan* plan, int64_t dims_out[3]);
+/* out = alpha * irfftn(symbol * rfftn(in)) [+ add] for ncomp (1 or 3) components */
+int vr_spec_apply(vr_spec_plan* plan, int kind, const float* in, int ncomp, double beta_v, double beta_w,
+                  double shift, double sigma, double alpha, const float* add, float* out, void* stream);
+/* prolong_spectral (grid.py:181-226): `in` on plan_coarse's grid (ncomp
+ * components) -> `out` on plan_fine's grid (each fine dim >= coarse dim). */
+int vr_prolong_spectral(vr_spec_plan* plan_coarse, vr_spec_plan* plan_fine, const float* in, int ncomp,
+                        float* out, void* stream);
+/* h1_energy (diffops.py:149-154) -> *out_dev */
+int vr_h1_energy(vr_spec_plan* plan, const float* f, double* out_dev, void* stream);
+
+/* ---- reductions (optim.py:80-85,231-258; grid.py:129-130) -----------------
+ * scratch: device f64 buffer of vr_reduce_scratch_doubles() entries. */
+int vr_reduce_scratch_doubles(void);
+/* out[q] = sum_i a[q][i]*b[q][i], q < k <= 4 (a, b: HOST arrays of device ptrs) */
+int vr_dots(int k, const float* const* a, const float* const* b, int64_t n, double* scratch, double* out,
+            void* stream);
+/* out2 = {sum (a-b)^2, sum (c-b)^2} (c may be NULL) -- relative_residual */
+int vr_sqdiff(const float* a, const float* b, const float* c, int64_t n, double* scratch, double* out2,
+              void* stream);
+/* out4 = {min a, max a, min b, max b} -- _intensity_shift, J extrema */
+int vr_minmax(const float* a, const float* b, int64_t n, double* scratch, double* out4, void* stream);
+/* out4 = {-max|v|^2, max|v|^2, #non-finite, #non-zero} over a 3 x n field */
+int vr_vecstats(const float* v, int64_t n, double* scratch, double* out4, void* stream);
+
+/* ---- vector updates --------------------------------------------------------- */
+int vr_axpby(int64_t n, double a, const float* x, double b, const float* y, float* out, void* stream);
+int vr_pcg_update(int64_t n, double alpha, const float* p, const float* hp, float* x, float* r, void* stream);
+int vr_fill(int64_t n, float value, float* out, void* stream);
+
+/* ---- Dice counts (metrics.py:45-57,72-73) ------------------------------------
+ * counts[3*id+{0,1,2}] = |l0==id|, |l1==id|, |l0==id & l1==id|, id <= max_id */
+int vr_label_counts(const int* l0, const int* l1, int64_t n, int max_id, unsigned long long* counts,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VELREG_B200_H */

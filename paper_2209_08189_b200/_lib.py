@@ -1,0 +1,208 @@
+"""ctypes binding of libvelreg_b200.so (the C ABI in include/velreg_b200.h).
+
+There is no fallback: if the shared library cannot be loaded, or no CUDA device
+is present, every operator raises.  torch provides device memory, the current
+stream and (for multi-GPU) the process group; all arithmetic on the hot path is
+in the hand-written sm_100a kernels behind this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from .errors import VelregError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvelreg_b200.so")
+
+_lib = None
+_lock = threading.Lock()
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int
+_f64 = C.c_double
+_f32 = C.c_float
+_dims_t = C.POINTER(C.c_int64)
+
+_SIGS = {
+    "vr_interp_points": [_p, _dims_t, _p, _i32, _i64, _i32, _p, _p],
+    "vr_trace_rk2": [_p, _dims_t, _f64, _i32, _p, _p, _p, _p, _p, _p],
+    "vr_disp_to_points": [_p, _dims_t, _p, _p],
+    "vr_advect": [_p, _dims_t, _p, _p, _i32, _p, _p, _p],
+    "vr_incstate_init": [_p, _p, _dims_t, _f64, _p, _p],
+    "vr_incstate_step": [_p, _dims_t, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
+    "vr_body_force": [_p, _p, _i32, _dims_t, _f64, _p, _p],
+    "vr_label_step": [_p, _p, _i32, _dims_t, _p, _i32, _p, _p, _p],
+    "vr_fd8_grad": [_p, _dims_t, _p, _p],
+    "vr_fd8_div": [_p, _dims_t, _p, _p],
+    "vr_spec_plan_create": [_dims_t, C.POINTER(_p)],
+    "vr_spec_plan_destroy": [_p],
+    "vr_spec_plan_dims": [_p, _dims_t],
+    "vr_spec_apply": [_p, _i32, _p, _i32, _f64, _f64, _f64, _f64, _f64, _p, _p, _p],
+    "vr_h1_energy": [_p, _p, _p, _p],
+    "vr_prolong_spectral": [_p, _p, _p, _i32, _p, _p],
+    "vr_reduce_scratch_doubles": [],
+    "vr_dots": [_i32, C.POINTER(_p), C.POINTER(_p), _i64, _p, _p, _p],
+    "vr_sqdiff": [_p, _p, _p, _i64, _p, _p, _p],
+    "vr_minmax": [_p, _p, _i64, _p, _p, _p],
+    "vr_vecstats": [_p, _i64, _p, _p, _p],
+    "vr_axpby": [_i64, _f64, _p, _f64, _p, _p, _p],
+    "vr_pcg_update": [_i64, _f64, _p, _p, _p, _p, _p],
+    "vr_fill": [_i64, _f32, _p, _p],
+    "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
+}
+
+EXPORTED = tuple(_SIGS)
+
+ORDER = {"linear": 1, "cubic": 3}
+SPEC_IDENTITY, SPEC_A, SPEC_INVSHIFT, SPEC_K, SPEC_GAUSS, SPEC_A2, SPEC_INVSHIFT2 = range(7)
+
+_ERRS = {-1: "invalid argument", -2: "invalid dims", -3: "kernel launch failed",
+         -4: "device allocation failed", -5: "unsupported configuration"}
+
+
+class NativeError(VelregError):
+    """The CUDA library rejected a call (bad arguments or launch failure)."""
+
+
+# kernels launched per C-ABI call (for the bench's gpu_launches accounting)
+LAUNCHES = {"vr_spec_apply": 5, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2,
+            "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
+            "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0}
+
+
+class Profile:
+    """Opt-in accounting used by bench.py: counts kernel launches per entry point
+    and brackets the entries named in `timed` with CUDA events on the launching
+    stream."""
+
+    def __init__(self):
+        self.enabled = False
+        self.timed: set = set()
+        self.launches: dict = {}
+        self.events: dict = {}
+
+    def reset(self, timed=()):
+        self.launches = {}
+        self.events = {n: [] for n in timed}
+        self.timed = set(timed)
+
+    def total_launches(self) -> int:
+        return sum(self.launches.values())
+
+    def avg_ms(self, name: str) -> tuple:
+        evs = self.events.get(name, [])
+        if not evs:
+            return 0.0, 0
+        torch.cuda.synchronize()
+        tot = sum(a.elapsed_time(b) for a, b in evs)
+        return tot / len(evs), len(evs)
+
+
+PROFILE = Profile()
+
+
+class _Bound:
+    def __init__(self, lib):
+        self._raw = lib
+        for name in _SIGS:
+            setattr(self, name, self._wrap(name, getattr(lib, name)))
+
+    @staticmethod
+    def _wrap(name, fn):
+        n_launch = LAUNCHES.get(name, 1)
+
+        def call(*args):
+            prof = PROFILE
+            if not prof.enabled:
+                return fn(*args)
+            if name in prof.timed:
+                s = torch.cuda.current_stream()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                rc = fn(*args)
+                b.record(s)
+                prof.events[name].append((a, b))
+            else:
+                rc = fn(*args)
+            prof.launches[name] = prof.launches.get(name, 0) + n_launch
+            return rc
+
+        call.__name__ = name
+        return call
+
+
+def load_library(path: str = LIB_PATH):
+    """Load (without requiring a GPU) and bind every exported symbol."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"{path} is missing: build it with `python -m paper_2209_08189_b200.build` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = _Bound(lib)
+        return _lib
+
+
+def lib():
+    if _lib is None:
+        load_library()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2209_08189_b200 needs a CUDA device (sm_100a); none is available "
+                           "and there is no CPU fallback")
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what}: {_ERRS.get(rc, 'error')} (code {rc})")
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def dims_arg(dims) -> C.Array:
+    return (C.c_int64 * 3)(*[int(n) for n in dims])
+
+
+def device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---- per-device scratch for reductions -------------------------------------
+_scratch: dict = {}
+
+
+def scratch() -> torch.Tensor:
+    dev = torch.cuda.current_device()
+    t = _scratch.get(dev)
+    if t is None:
+        n = lib().vr_reduce_scratch_doubles()
+        t = torch.empty(n, dtype=torch.float64, device=device())
+        _scratch[dev] = t
+    return t
+
+
+def out_buf(n: int) -> torch.Tensor:
+    return torch.empty(n, dtype=torch.float64, device=device())
+
+
+def ptr_array(ts) -> C.Array:
+    return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])

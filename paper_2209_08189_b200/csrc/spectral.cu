@@ -1,0 +1,708 @@
+// Spectral operators on hand-written batched mixed-radix FFT stages.
+//
+// Reference: /root/reference/pkg/src/velreg/diffops.py
+//   SpectralWorkspace (:24-55)  -> vr_spec_plan (wavenumbers, rfft layout, multiplicity)
+//   apply_A (:116-118)          -> SPEC_A      symbol |k|^2
+//   apply_inv_shifted_A (:121)  -> SPEC_INVSHIFT symbol 1/(beta_v |k|^2 + shift)
+//   apply_K (:129-146)          -> SPEC_K      Leray blend (couples the 3 components)
+//   h1_energy (:149-154)        -> vr_h1_energy (forward transform + weighted reduction)
+// numpy's rfftn/irfftn(s=dims) are pocketfft; this file re-derives the same
+// transforms as a 3-pass pipeline per component:
+//   Z  : real rows (x3) -> half spectrum (n3/2+1), f64           [fwd_z_kernel]
+//   Y  : c2c along x2 (strided tiles staged in smem), f64         [y_kernel]
+//   X  : c2c along x1 forward, operator multiply, c2c inverse, all
+//        in one kernel (the operator is diagonal in k)             [x_op_kernel]
+//   Y' : c2c inverse along x2, f32                                [y_kernel]
+//   Z' : Hermitian c2r along x3 (imag of DC/Nyquist dropped, as pocketfft's
+//        c2r does), f32, with a fused "+ addend" epilogue        [inv_z_kernel]
+// The forward half runs in f64 (storage + arithmetic): the |k|^2 symbol
+// amplifies absolute rounding at high k, and an f32 forward path cannot meet the
+// 1e-5 operator tolerance at 256^3.  After the multiply the
+// output is O(|A v|) so the inverse half runs in f32.
+//
+// Each line FFT is an out-of-place Stockham DIT over shared memory; radices
+// 8/4/2 (powers of two), 3/5/7 (register butterflies) and any other prime via a
+// direct O(R) stage, so every even grid size the reference accepts works
+// (e.g. the CLARITY sizes 2816 = 2^8*11, 3016 = 2^3*13*29, 1162 = 2*7*83).
+#include <vector>
+#include <new>
+#include "common.cuh"
+#include "../../include/velreg_b200.h"
+
+namespace vr {
+
+struct RadixPlan {
+  int L;
+  int ns;
+  int r[24];
+};
+
+static RadixPlan make_radix_plan(int L) {
+  RadixPlan p{};
+  p.L = L;
+  int m = L;
+  const int pref[3] = {8, 4, 2};
+  for (int q : pref)
+    while (m % q == 0) { p.r[p.ns++] = q; m /= q; }
+  for (int q = 3; m > 1; q += 2)
+    while (m % q == 0) { p.r[p.ns++] = q; m /= q; }
+  return p;
+}
+
+// ---- complex helpers -------------------------------------------------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <typename C> __device__ __forceinline__ C cvt(double2 w);
+template <> __device__ __forceinline__ double2 cvt<double2>(double2 w) { return w; }
+template <> __device__ __forceinline__ float2 cvt<float2>(double2 w) { return make_float2((float)w.x, (float)w.y); }
+template <typename C> __device__ __forceinline__ C cvt_from(double2 w) { return cvt<C>(w); }
+__device__ __forceinline__ double2 to_d(float2 a) { return make_double2(a.x, a.y); }
+__device__ __forceinline__ double2 to_d(double2 a) { return a; }
+// multiply by -i (forward) or +i (inverse)
+template <typename C> __device__ __forceinline__ C rot(C a, bool inv) {
+  C r;
+  if (inv) { r.x = -a.y; r.y = a.x; } else { r.x = a.y; r.y = -a.x; }
+  return r;
+}
+// twiddle W^m (forward e^{-2 pi i m/L}; inverse is the conjugate)
+template <typename C> __device__ __forceinline__ C twid(const double2* tw, int m, bool inv) {
+  double2 w = tw[m];
+  if (inv) w.y = -w.y;
+  return cvt<C>(w);
+}
+
+template <typename C>
+__device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3, bool inv) {
+  C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = rot(csub(a1, a3), inv);
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+
+template <typename C, int R>
+__device__ __forceinline__ void dft_reg(C* v, const double2* tw, int L, bool inv) {
+  if (R == 2) {
+    C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if (R == 4) {
+    dft4(v[0], v[1], v[2], v[3], inv);
+  } else if (R == 8) {
+    C e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    C o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4(e0, e1, e2, e3, inv);
+    dft4(o0, o1, o2, o3, inv);
+    const double s = 0.70710678118654752440;
+    // W8^1 = s(1 -+ i), W8^2 = -+i, W8^3 = s(-1 -+ i)
+    C w1, w3;
+    w1.x = s; w1.y = inv ? s : -s;
+    w3.x = -s; w3.y = inv ? s : -s;
+    o1 = cmul(o1, w1);
+    o2 = rot(o2, inv);
+    o3 = cmul(o3, w3);
+    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+    v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
+    v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
+    v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
+  } else {
+    // small odd radix: direct DFT with the line's twiddle table (W_R = W_L^(L/R))
+    C out[R];
+    const int st = L / R;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      C acc = v[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], twid<C>(tw, ((r * s) % R) * st, inv)));
+      out[s] = acc;
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = out[s];
+  }
+}
+
+template <typename C, int R>
+__device__ __forceinline__ void stage_reg(const C* __restrict__ src, C* __restrict__ dst, int L, int nb, int j,
+                                          int Ns, const double2* tw, bool inv) {
+  const int k = j % Ns;
+  const int st = L / (Ns * R);
+  C v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    v[r] = src[j + r * nb];
+    if (r > 0 && k > 0) v[r] = cmul(v[r], twid<C>(tw, r * k * st, inv));
+  }
+  dft_reg<C, R>(v, tw, L, inv);
+  const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) dst[idxD + r * Ns] = v[r];
+}
+
+template <typename C>
+__device__ void stage_generic(const C* __restrict__ src, C* __restrict__ dst, int L, int R, int nb, int j, int Ns,
+                              const double2* tw, bool inv) {
+  const int k = j % Ns;
+  const int st = L / (Ns * R);
+  const int sR = L / R;
+  const int idxD = (j / Ns) * Ns * R + k;
+  for (int s = 0; s < R; ++s) {
+    C acc = src[j];
+    for (int r = 1; r < R; ++r) {
+      C x = src[j + r * nb];
+      if (k > 0) x = cmul(x, twid<C>(tw, r * k * st, inv));
+      acc = cadd(acc, cmul(x, twid<C>(tw, ((r * s) % R) * sR, inv)));
+    }
+    dst[idxD + s * Ns] = acc;
+  }
+}
+
+// nl lines of length L (line stride ls) in `a`; `b` is scratch of the same
+// shape.  Returns the buffer holding the (naturally ordered) result.
+template <typename C>
+__device__ C* line_fft(C* a, C* b, int ls, int nl, const RadixPlan& rp, const double2* tw, bool inv) {
+  const int L = rp.L;
+  int Ns = 1;
+  for (int s = 0; s < rp.ns; ++s) {
+    const int R = rp.r[s];
+    const int nb = L / R;
+    const int total = nl * nb;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int line = t / nb, j = t - line * nb;
+      const C* src = a + line * ls;
+      C* dst = b + line * ls;
+      switch (R) {
+        case 2: stage_reg<C, 2>(src, dst, L, nb, j, Ns, tw, inv); break;
+        case 4: stage_reg<C, 4>(src, dst, L, nb, j, Ns, tw, inv); break;
+        case 8: stage_reg<C, 8>(src, dst, L, nb, j, Ns, tw, inv); break;
+        case 3: stage_reg<C, 3>(src, dst, L, nb, j, Ns, tw, inv); break;
+        case 5: stage_reg<C, 5>(src, dst, L, nb, j, Ns, tw, inv); break;
+        case 7: stage_reg<C, 7>(src, dst, L, nb, j, Ns, tw, inv); break;
+        default: stage_generic<C>(src, dst, L, R, nb, j, Ns, tw, inv); break;
+      }
+    }
+    __syncthreads();
+    C* t = a; a = b; b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void load_twiddles(double2* tw_s, const double2* __restrict__ tw, int L) {
+  for (int t = threadIdx.x; t < L; t += blockDim.x) tw_s[t] = tw[t];
+}
+
+// ---- operator symbols (applied between the forward and inverse x1 passes) ----
+struct SpecOp {
+  int kind;
+  int ncomp;
+  double beta_v, beta_w, shift, scale, sigma;
+};
+
+__device__ __forceinline__ int signed_freq(int m, int n) { return m < n / 2 ? m : m - n; }  // fftfreq*n
+
+// vals[c] for c < op.ncomp at wavenumber (k1,k2,k3); result in place.
+__device__ __forceinline__ void apply_symbol(const SpecOp& op, double k1, double k2, double k3, double2* vals) {
+  const double ksq = k1 * k1 + k2 * k2 + k3 * k3;  // diffops.py:38 (exact integers)
+  switch (op.kind) {
+    case VR_SPEC_A: {  // diffops.py:116-118
+      const double m = ksq * op.scale;
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= m; vals[c].y *= m; }
+    } break;
+    case VR_SPEC_INVSHIFT: {  // diffops.py:121-126
+      const double m = (1.0 / (op.beta_v * ksq + op.shift)) * op.scale;
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= m; vals[c].y *= m; }
+    } break;
+    case VR_SPEC_K: {  // diffops.py:129-146
+      if (ksq > 0.0) {
+        const double a = ksq, b = 1.0 + ksq;
+        const double cb = (op.beta_w * b) / (op.beta_v * a + op.beta_w * b);
+        const double2 kd = make_double2(k1 * vals[0].x + k2 * vals[1].x + k3 * vals[2].x,
+                                        k1 * vals[0].y + k2 * vals[1].y + k3 * vals[2].y);
+        const double f = cb * (1.0 / ksq);
+        const double2 sc = make_double2(f * kd.x, f * kd.y);
+        const double kk[3] = {k1, k2, k3};
+        for (int c = 0; c < 3; ++c) {
+          vals[c].x = (vals[c].x - kk[c] * sc.x) * op.scale;
+          vals[c].y = (vals[c].y - kk[c] * sc.y) * op.scale;
+        }
+      } else {
+        for (int c = 0; c < 3; ++c) { vals[c].x *= op.scale; vals[c].y *= op.scale; }
+      }
+    } break;
+    case VR_SPEC_GAUSS: {  // Gaussian smoothing exp(-sigma^2 |k|^2 / 2) (north-star extra)
+      const double m = exp(-0.5 * op.sigma * op.sigma * ksq) * op.scale;
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= m; vals[c].y *= m; }
+    } break;
+    case VR_SPEC_A2: {  // H2 seminorm operator, symbol |k|^4 (north-star extra)
+      const double m = ksq * ksq * op.scale;
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= m; vals[c].y *= m; }
+    } break;
+    case VR_SPEC_INVSHIFT2: {  // inverse of beta_v A2 + shift
+      const double m = (1.0 / (op.beta_v * ksq * ksq + op.shift)) * op.scale;
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= m; vals[c].y *= m; }
+    } break;
+    default: {  // VR_SPEC_IDENTITY: pure round trip
+      for (int c = 0; c < op.ncomp; ++c) { vals[c].x *= op.scale; vals[c].y *= op.scale; }
+    }
+  }
+}
+
+// ---- pass kernels ---------------------------------------------------------------
+// Z forward: real rows -> half spectrum (f64).  grid (ceil(rows/RB), ncomp)
+__global__ void __launch_bounds__(256) fwd_z_kernel(const float* __restrict__ in, Dims d, int n3h, RadixPlan rp,
+                                                    const double2* __restrict__ tw, int RB,
+                                                    double2* __restrict__ S) {
+  extern __shared__ double2 smd[];
+  const int L = d.n3, ls = L + 1;
+  double2* tw_s = smd;
+  double2* a = tw_s + L;
+  double2* b = a + RB * ls;
+  load_twiddles(tw_s, tw, L);
+  const int nrows = d.n1 * d.n2;
+  const int row0 = blockIdx.x * RB;
+  const int nr = min(RB, nrows - row0);
+  const int c = blockIdx.y;
+  const float* src = in + (int64_t)c * d.n() + (int64_t)row0 * L;
+  for (int t = threadIdx.x; t < nr * L; t += blockDim.x) {
+    const int r = t / L, k = t - r * L;
+    a[r * ls + k] = make_double2((double)__ldg(src + t), 0.0);
+  }
+  __syncthreads();
+  double2* res = line_fft<double2>(a, b, ls, nr, rp, tw_s, false);
+  double2* dst = S + (int64_t)c * d.n1 * d.n2 * n3h + (int64_t)row0 * n3h;
+  for (int t = threadIdx.x; t < nr * n3h; t += blockDim.x) {
+    const int r = t / n3h, k = t - r * n3h;
+    dst[t] = res[r * ls + k];
+  }
+}
+
+// Strided-axis c2c pass in place on C-typed spectra (the Y pass, and the plain
+// X pass used by resampling).  Lines of length L with element stride `es`;
+// `n_outer` independent line sets `outer_stride` apart; B consecutive kz per
+// CTA so the global reads are B*sizeof(C)-byte contiguous segments.
+// grid (n_outer*nchunks, ncomp)
+template <typename C>
+__global__ void __launch_bounds__(256) axis_kernel(C* __restrict__ S, int L, int64_t es, int n_outer,
+                                                   int64_t outer_stride, int64_t comp_stride, int n3h,
+                                                   RadixPlan rp, const double2* __restrict__ tw, int B, int inv) {
+  extern __shared__ double2 smd[];
+  const int ls = L + 1;
+  double2* tw_s = smd;
+  C* a = reinterpret_cast<C*>(tw_s + L);
+  C* b = a + B * ls;
+  load_twiddles(tw_s, tw, L);
+  const int nchunks = (n3h + B - 1) / B;
+  const int o = blockIdx.x / nchunks, kz0 = (blockIdx.x - o * nchunks) * B;
+  const int nb = min(B, n3h - kz0);
+  C* base = S + blockIdx.y * comp_stride + o * outer_stride + kz0;
+  for (int t = threadIdx.x; t < L * nb; t += blockDim.x) {
+    const int j = t / nb, q = t - j * nb;
+    a[q * ls + j] = base[j * es + q];
+  }
+  __syncthreads();
+  C* res = line_fft<C>(a, b, ls, nb, rp, tw_s, inv != 0);
+  for (int t = threadIdx.x; t < L * nb; t += blockDim.x) {
+    const int j = t / nb, q = t - j * nb;
+    base[j * es + q] = res[q * ls + j];
+  }
+}
+
+// Spectral zero-padding for prolongation (grid.py:181-208): every fine mode
+// takes the coarse mode it maps to along each axis, halving at the two split
+// Nyquist positions; the x3 (half) axis keeps only the positive Nyquist half,
+// its mirror being implied by Hermitian symmetry in the c2r pass.  Scaled by
+// 1/N_coarse (= N_t/N_s product scale times the 1/N_t inverse normalisation).
+__device__ __forceinline__ int pad_src(int t, int ns, int nt, double& w) {
+  w = 1.0;
+  if (nt == ns) return t;
+  const int half = ns / 2;
+  if (t < half) return t;
+  if (t == half || t == nt - half) { w = 0.5; return half; }
+  if (t > nt - half) return t - nt + ns;
+  w = 0.0;
+  return 0;
+}
+
+__global__ void pad_kernel(const double2* __restrict__ Sc, Dims dc, int n3hc, float2* __restrict__ Tf, Dims df,
+                           int n3hf, int ncomp, double scale) {
+  const int64_t nspec_f = (int64_t)df.n1 * df.n2 * n3hf;
+  const int64_t nspec_c = (int64_t)dc.n1 * dc.n2 * n3hc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nspec_f * ncomp;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / nspec_f);
+    int64_t r = e - c * nspec_f;
+    const int kz = (int)(r % n3hf);
+    r /= n3hf;
+    const int j = (int)(r % df.n2), i = (int)(r / df.n2);
+    double w1, w2, w3 = 1.0;
+    const int si = pad_src(i, dc.n1, df.n1, w1), sj = pad_src(j, dc.n2, df.n2, w2);
+    int sk = kz;
+    if (df.n3 != dc.n3) {
+      const int half = dc.n3 / 2;
+      if (kz < half) sk = kz;
+      else if (kz == half) { sk = half; w3 = 0.5; }
+      else { sk = 0; w3 = 0.0; }
+    }
+    const double w = w1 * w2 * w3 * scale;
+    float2 out = make_float2(0.f, 0.f);
+    if (w != 0.0) {
+      const double2 v = Sc[c * nspec_c + ((int64_t)si * dc.n2 + sj) * n3hc + sk];
+      out = make_float2((float)(w * v.x), (float)(w * v.y));
+    }
+    Tf[e] = out;
+  }
+}
+
+// X pass: forward c2c (f64) -> symbol -> inverse c2c (f64) -> store f32 into T.
+// REDUCE: instead, accumulate the H1 energy sum mult*(1+|k|^2)*|F|^2 (diffops.py:149-154).
+template <bool REDUCE>
+__global__ void __launch_bounds__(256) x_op_kernel(const double2* __restrict__ S, float2* __restrict__ T, Dims d,
+                                                   int n3h, RadixPlan rp, const double2* __restrict__ tw, int B,
+                                                   SpecOp op, double* __restrict__ partials) {
+  extern __shared__ double2 smd[];
+  const int L = d.n1, ls = L + 1, NC = op.ncomp;
+  double2* tw_s = smd;
+  double2* a = tw_s + L;
+  double2* b = a + NC * B * ls;
+  load_twiddles(tw_s, tw, L);
+  const int nchunks = (n3h + B - 1) / B;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * B;
+  const int nb = min(B, n3h - kz0);
+  const int64_t cstride = (int64_t)d.n1 * d.n2 * n3h;
+  const int64_t lstride = (int64_t)d.n2 * n3h;
+  const double2* sbase = S + (int64_t)j * n3h + kz0;
+  for (int t = threadIdx.x; t < NC * L * nb; t += blockDim.x) {
+    const int c = t / (L * nb);
+    const int r = t - c * L * nb;
+    const int i = r / nb, q = r - i * nb;
+    a[(c * B + q) * ls + i] = sbase[c * cstride + i * lstride + q];
+  }
+  // unused lines (q >= nb) are left untouched; they never reach memory
+  __syncthreads();
+  double2* res = line_fft<double2>(a, b, ls, NC * B, rp, tw_s, false);
+  double2* other = (res == a) ? b : a;
+  const double k2 = (double)signed_freq(j, d.n2);
+  if (REDUCE) {
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < L * nb; t += blockDim.x) {
+      const int q = t / L, m = t - q * L;
+      const double k1 = (double)signed_freq(m, d.n1), k3 = (double)(kz0 + q);
+      const double ksq = k1 * k1 + k2 * k2 + k3 * k3;
+      const int kz = kz0 + q;
+      const double mult = (kz == 0 || (d.n3 % 2 == 0 && kz == n3h - 1)) ? 1.0 : 2.0;  // diffops.py:45-49
+      const double2 v = res[q * ls + m];
+      acc += mult * (1.0 + ksq) * (v.x * v.x + v.y * v.y);
+    }
+    // deterministic block reduction
+    __shared__ double red[32];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      x = warp_sum(x);
+      if (threadIdx.x == 0) partials[blockIdx.x] = x;
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < L * nb; t += blockDim.x) {
+    const int q = t / L, m = t - q * L;
+    const double k1 = (double)signed_freq(m, d.n1), k3 = (double)(kz0 + q);
+    double2 vals[3];
+    for (int c = 0; c < NC; ++c) vals[c] = res[(c * B + q) * ls + m];
+    apply_symbol(op, k1, k2, k3, vals);
+    for (int c = 0; c < NC; ++c) res[(c * B + q) * ls + m] = vals[c];
+  }
+  __syncthreads();
+  double2* out = line_fft<double2>(res, other, ls, NC * B, rp, tw_s, true);
+  float2* tbase = T + (int64_t)j * n3h + kz0;
+  for (int t = threadIdx.x; t < NC * L * nb; t += blockDim.x) {
+    const int c = t / (L * nb);
+    const int r = t - c * L * nb;
+    const int i = r / nb, q = r - i * nb;
+    const double2 v = out[(c * B + q) * ls + i];
+    tbase[c * cstride + i * lstride + q] = make_float2((float)v.x, (float)v.y);
+  }
+}
+
+// Z inverse: Hermitian half rows (f32) -> real rows, out = x (+ add).
+__global__ void __launch_bounds__(256) inv_z_kernel(const float2* __restrict__ T, Dims d, int n3h, RadixPlan rp,
+                                                    const double2* __restrict__ tw, int RB,
+                                                    float* __restrict__ out, const float* __restrict__ add) {
+  extern __shared__ double2 smd[];
+  const int L = d.n3, ls = L + 1;
+  double2* tw_s = smd;
+  float2* a = reinterpret_cast<float2*>(tw_s + L);
+  float2* b = a + RB * ls;
+  load_twiddles(tw_s, tw, L);
+  const int nrows = d.n1 * d.n2;
+  const int row0 = blockIdx.x * RB;
+  const int nr = min(RB, nrows - row0);
+  const int c = blockIdx.y;
+  const float2* src = T + (int64_t)c * nrows * n3h + (int64_t)row0 * n3h;
+  for (int t = threadIdx.x; t < nr * n3h; t += blockDim.x) {
+    const int r = t / n3h, k = t - r * n3h;
+    float2 v = src[t];
+    if (k == 0 || (k == n3h - 1 && (L % 2 == 0))) v.y = 0.0f;  // c2r ignores imag of DC/Nyquist
+    a[r * ls + k] = v;
+    if (k > 0 && L - k > k) a[r * ls + (L - k)] = make_float2(v.x, -v.y);
+  }
+  __syncthreads();
+  float2* res = line_fft<float2>(a, b, ls, nr, rp, tw_s, true);
+  const int64_t off = (int64_t)c * d.n() + (int64_t)row0 * L;
+  for (int t = threadIdx.x; t < nr * L; t += blockDim.x) {
+    const int r = t / L, k = t - r * L;
+    float v = res[r * ls + k].x;
+    if (add) v += __ldg(add + off + t);
+    out[off + t] = v;
+  }
+}
+
+__global__ void finalize_sum_kernel(const double* __restrict__ partials, int n, double scale,
+                                    double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) acc += partials[t];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    x = warp_sum(x);
+    if (threadIdx.x == 0) *out = x * scale;
+  }
+}
+
+}  // namespace vr
+
+using namespace vr;
+
+struct vr_spec_plan {
+  Dims d;
+  int n3h;
+  int64_t nspec;  // n1*n2*n3h
+  RadixPlan rp1, rp2, rp3;
+  double2 *tw1, *tw2, *tw3;
+  double2* S;      // 3 * nspec (forward, f64)
+  float2* T;       // 3 * nspec (inverse, f32)
+  double* partials;
+  int RBz, RBzi, By, Byi, Bx1, Bx3;
+  size_t smz, smzi, smy, smyi, smx1, smx3;
+  int device;
+};
+
+namespace {
+
+int pow2_floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+int choose_lines(int L, int ncomp, size_t elem, size_t budget, int cap) {
+  int B = (int)(budget / (2 * (size_t)ncomp * (L + 1) * elem));
+  if (B < 1) B = 1;
+  B = pow2_floor(B);
+  return B > cap ? cap : B;
+}
+
+int upload_twiddles(int L, double2** out) {
+  std::vector<double2> h(L);
+  for (int m = 0; m < L; ++m) {
+    // e^{-2 pi i m / L}; reduce the angle to the first octant-friendly range
+    double ang = -kTwoPi * (double)m / (double)L;
+    h[m] = make_double2(cos(ang), sin(ang));
+  }
+  if (cudaMalloc(out, sizeof(double2) * L) != cudaSuccess) return VR_ERR_ALLOC;
+  if (cudaMemcpy(*out, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) return VR_ERR_ALLOC;
+  return VR_OK;
+}
+
+const size_t kSmemBudget = 200 * 1024;
+
+}  // namespace
+
+extern "C" {
+
+int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
+  if (!out) return VR_ERR_ARG;
+  *out = nullptr;
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (d.n1 < 2 || d.n2 < 2 || d.n3 < 2 || (d.n3 % 2)) return VR_ERR_DIMS;
+  vr_spec_plan* p = new (std::nothrow) vr_spec_plan();
+  if (!p) return VR_ERR_ALLOC;
+  p->d = d;
+  p->n3h = d.n3 / 2 + 1;
+  p->nspec = (int64_t)d.n1 * d.n2 * p->n3h;
+  p->rp1 = make_radix_plan(d.n1);
+  p->rp2 = make_radix_plan(d.n2);
+  p->rp3 = make_radix_plan(d.n3);
+  cudaGetDevice(&p->device);
+  rc = upload_twiddles(d.n1, &p->tw1);
+  if (!rc) rc = upload_twiddles(d.n2, &p->tw2);
+  if (!rc) rc = upload_twiddles(d.n3, &p->tw3);
+  if (!rc && cudaMalloc(&p->S, sizeof(double2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
+  if (!rc && cudaMalloc(&p->T, sizeof(float2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
+  const int maxblk = d.n2 * p->n3h + 1024;
+  if (!rc && cudaMalloc(&p->partials, sizeof(double) * maxblk) != cudaSuccess) rc = VR_ERR_ALLOC;
+  if (rc) {
+    vr_spec_plan_destroy(p);
+    return rc;
+  }
+  // tile shapes: ~2-4K complex elements per CTA, within the smem budget
+  const size_t kLines = 4096;
+  p->RBz = (int)std::max<size_t>(1, std::min<size_t>(16, kLines / d.n3));
+  p->RBzi = p->RBz;
+  p->smz = sizeof(double2) * (d.n3 + 2 * (size_t)p->RBz * (d.n3 + 1));
+  p->smzi = sizeof(double2) * d.n3 + sizeof(float2) * 2 * (size_t)p->RBzi * (d.n3 + 1);
+  p->By = std::min(choose_lines(d.n2, 1, sizeof(double2), 110 * 1024, 16), pow2_floor(p->n3h));
+  p->Byi = std::min(choose_lines(d.n2, 1, sizeof(float2), 110 * 1024, 16), pow2_floor(p->n3h));
+  p->smy = sizeof(double2) * (d.n2 + 2 * (size_t)p->By * (d.n2 + 1));
+  p->smyi = sizeof(double2) * d.n2 + sizeof(float2) * 2 * (size_t)p->Byi * (d.n2 + 1);
+  p->Bx3 = std::min(choose_lines(d.n1, 3, sizeof(double2), 110 * 1024, 8), pow2_floor(p->n3h));
+  p->Bx1 = std::min(choose_lines(d.n1, 1, sizeof(double2), 110 * 1024, 16), pow2_floor(p->n3h));
+  p->smx3 = sizeof(double2) * (d.n1 + 2 * 3 * (size_t)p->Bx3 * (d.n1 + 1));
+  p->smx1 = sizeof(double2) * (d.n1 + 2 * 1 * (size_t)p->Bx1 * (d.n1 + 1));
+  if (p->smz > kSmemBudget || p->smzi > kSmemBudget || p->smy > kSmemBudget || p->smyi > kSmemBudget ||
+      p->smx3 > kSmemBudget || p->smx1 > kSmemBudget) {
+    vr_spec_plan_destroy(p);
+    return VR_ERR_UNSUPPORTED;
+  }
+  cudaFuncSetAttribute(fwd_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  cudaFuncSetAttribute(inv_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  cudaFuncSetAttribute(axis_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  cudaFuncSetAttribute(axis_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  cudaFuncSetAttribute(x_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  cudaFuncSetAttribute(x_op_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  *out = p;
+  return VR_OK;
+}
+
+int vr_spec_plan_destroy(vr_spec_plan* p) {
+  if (!p) return VR_OK;
+  cudaFree(p->tw1);
+  cudaFree(p->tw2);
+  cudaFree(p->tw3);
+  cudaFree(p->S);
+  cudaFree(p->T);
+  cudaFree(p->partials);
+  delete p;
+  return VR_OK;
+}
+
+}  // extern "C"
+
+// strided c2c pass along x1 (axis 1) or x2 (axis 2) over ncomp spectra
+template <typename C>
+static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, cudaStream_t s) {
+  const Dims& d = p->d;
+  const bool ax2 = axis == 2;
+  const int L = ax2 ? d.n2 : d.n1;
+  const int64_t es = ax2 ? (int64_t)p->n3h : (int64_t)d.n2 * p->n3h;
+  const int n_outer = ax2 ? d.n1 : d.n2;
+  const int64_t outer_stride = ax2 ? (int64_t)d.n2 * p->n3h : (int64_t)p->n3h;
+  const int B = std::min(choose_lines(L, 1, sizeof(C), 110 * 1024, 16), pow2_floor(p->n3h));
+  const size_t sm = sizeof(double2) * L + sizeof(C) * 2 * (size_t)B * (L + 1);
+  const int nchunks = (p->n3h + B - 1) / B;
+  axis_kernel<C><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, L, es, n_outer, outer_stride, p->nspec,
+                                                                 p->n3h, ax2 ? p->rp2 : p->rp1,
+                                                                 ax2 ? p->tw2 : p->tw1, B, inv);
+}
+
+static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s) {
+  const Dims& d = p->d;
+  const int nrows = d.n1 * d.n2;
+  fwd_z_kernel<<<dim3((nrows + p->RBz - 1) / p->RBz, ncomp), 256, p->smz, s>>>(in, d, p->n3h, p->rp3, p->tw3,
+                                                                               p->RBz, p->S);
+  launch_axis<double2>(p, p->S, 2, ncomp, 0, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+static void spec_inverse_yz(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
+  const Dims& d = p->d;
+  launch_axis<float2>(p, p->T, 2, ncomp, 1, s);
+  const int nrows = d.n1 * d.n2;
+  inv_z_kernel<<<dim3((nrows + p->RBzi - 1) / p->RBzi, ncomp), 256, p->smzi, s>>>(p->T, d, p->n3h, p->rp3, p->tw3,
+                                                                                  p->RBzi, out, add);
+}
+
+extern "C" {
+
+// out = alpha * IFFT(symbol * FFT(in)) [+ add], component-wise or coupled (K).
+// alpha is folded into the f64 symbol (e.g. beta_v * A v + body in one call).
+int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double beta_v, double beta_w,
+                  double shift, double sigma, double alpha, const float* add, float* out, void* stream) {
+  if (!p || !in || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const Dims& d = p->d;
+  int rc = spec_forward(p, in, ncomp, s);
+  if (rc) return rc;
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma};
+  const int B = ncomp == 3 ? p->Bx3 : p->Bx1;
+  const size_t sm = ncomp == 3 ? p->smx3 : p->smx1;
+  const int ncx = (p->n3h + B - 1) / B;
+  x_op_kernel<false><<<d.n2 * ncx, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, nullptr);
+  spec_inverse_yz(p, ncomp, add, out, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// prolong_spectral (grid.py:181-226): coarse rfftn -> Nyquist-split zero pad ->
+// fine irfftn, all on the device; `in` lives on pc's grid, `out` on pf's.
+int vr_prolong_spectral(vr_spec_plan* pc, vr_spec_plan* pf, const float* in, int ncomp, float* out,
+                        void* stream) {
+  if (!pc || !pf || !in || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (pf->d.n1 < pc->d.n1 || pf->d.n2 < pc->d.n2 || pf->d.n3 < pc->d.n3) return VR_ERR_DIMS;
+  if (pc->d.n1 % 2 || pc->d.n2 % 2 || pc->d.n3 % 2) return VR_ERR_DIMS;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = spec_forward(pc, in, ncomp, s);
+  if (rc) return rc;
+  launch_axis<double2>(pc, pc->S, 1, ncomp, 0, s);
+  const int64_t n = pf->nspec * ncomp;
+  pad_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(pc->S, pc->d, pc->n3h, pf->T, pf->d, pf->n3h, ncomp,
+                                                          1.0 / (double)pc->d.n());
+  launch_axis<float2>(pf, pf->T, 1, ncomp, 1, s);
+  spec_inverse_yz(pf, ncomp, nullptr, out, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// (2 pi)^3 * sum mult (1+|k|^2) |F/N|^2  -> *out_dev (device f64)
+int vr_h1_energy(vr_spec_plan* p, const float* f, double* out_dev, void* stream) {
+  if (!p || !f || !out_dev) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const Dims& d = p->d;
+  int rc = spec_forward(p, f, 1, s);
+  if (rc) return rc;
+  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0};
+  const int B = p->Bx1;
+  const int ncx = (p->n3h + B - 1) / B;
+  const int nblk = d.n2 * ncx;
+  x_op_kernel<true><<<nblk, 256, p->smx1, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, p->partials);
+  const double n = (double)d.n();
+  finalize_sum_kernel<<<1, 1024, 0, s>>>(p->partials, nblk, kTwoPi * kTwoPi * kTwoPi / (n * n), out_dev);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_spec_plan_dims(const vr_spec_plan* p, int64_t dims_out[3]) {
+  if (!p || !dims_out) return VR_ERR_ARG;
+  dims_out[0] = p->d.n1;
+  dims_out[1] = p->d.n2;
+  dims_out[2] = p->d.n3;
+  return VR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,373 @@
+// Semi-Lagrangian transport kernels: scattered interpolation, RK2 trace,
+// trapezoidal source factors, and the state / adjoint / incremental-state /
+// Jacobian sweeps of /root/reference/pkg/src/velreg/transport.py.
+//
+// Characteristics are stored as DISPLACEMENTS in index units (12 B/voxel):
+// departure point of voxel (i,j,k) = (i-d1, j-d2, k-d3).  The reference stores
+// absolute radians wrapped to [0,2pi) (transport.py:75); both describe the same
+// point, the displacement keeps full fp32 precision for the interpolation
+// fraction at any grid size.
+#include "common.cuh"
+#include "interp.cuh"
+#include "../../include/velreg_b200.h"
+
+namespace vr {
+
+__device__ __forceinline__ void voxel_ijk(int idx, const Dims& d, int& i, int& j, int& k) {
+  k = idx % d.n3;
+  int r = idx / d.n3;
+  j = r % d.n2;
+  i = r / d.n2;
+}
+
+__device__ __forceinline__ void flag_nonfinite(int* flag, float v) {
+  if (flag && !isfinite(v)) atomicOr(flag, 1);
+}
+
+// ---- interpolate_values at absolute points in radians (interp.py:112-128) ----
+template <int ORDER, typename PT>
+__global__ void __launch_bounds__(256) interp_points_kernel(const float* __restrict__ src, Dims d,
+                                                            const PT* __restrict__ pts, int64_t npts,
+                                                            double h1, double h2, double h3,
+                                                            float* __restrict__ out) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  // index = p / h (interp.py:23-25), floor, fraction; computed in f64
+  double q1 = (double)pts[p] / h1, q2 = (double)pts[npts + p] / h2, q3 = (double)pts[2 * npts + p] / h3;
+  double f1 = floor(q1), f2 = floor(q2), f3 = floor(q3);
+  SrcF32 s{{src, src, src}, 0};
+  float o;
+  gather<ORDER, 1>(s, d, (int)f1, (int)f2, (int)f3, (float)(q1 - f1), (float)(q2 - f2), (float)(q3 - f3),
+                   &o);
+  out[p] = o;
+}
+
+// ---- RK2 (Heun) trace, both directions, optional source factors -------------
+// transport.py:66-76 (trace), :94-110 (TransportOperators factors):
+//   x* = x - dt v(x);  X = x - dt/2 (v(x) + v(x*))           (forward)
+//   backward trace is the same with -v (transport.py:102)
+//   jac = (1 + dt/2 div(X_f)) / (1 - dt/2 div(x)),  adj likewise with X_b
+template <int ORDER, bool FACTORS>
+__global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
+                                                    float ih2, float ih3, float* __restrict__ disp_f,
+                                                    float* __restrict__ disp_b,
+                                                    const float* __restrict__ div,
+                                                    float* __restrict__ fac_f, float* __restrict__ fac_b) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  const float v1 = __ldg(v + idx), v2 = __ldg(v + N + idx), v3 = __ldg(v + 2 * N + idx);
+  const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
+  SrcF32 sv{{v, v + N, v + 2 * N}, N};
+  float vs[3];
+  const float half = 0.5f * dt;
+  // forward: x* = x - dt v
+  gather_disp<ORDER, 3>(sv, d, i, j, k, a1, a2, a3, vs);
+  const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
+  disp_f[idx] = f1;
+  disp_f[N + idx] = f2;
+  disp_f[2 * N + idx] = f3;
+  // backward: x* = x + dt v, X = x + dt/2 (v + v(x*))
+  gather_disp<ORDER, 3>(sv, d, i, j, k, -a1, -a2, -a3, vs);
+  const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
+  disp_b[idx] = b1;
+  disp_b[N + idx] = b2;
+  disp_b[2 * N + idx] = b3;
+  if (FACTORS) {
+    SrcF32 sd{{div, div, div}, 0};
+    const float denom = 1.0f - half * __ldg(div + idx);
+    float dv;
+    gather_disp<ORDER, 1>(sd, d, i, j, k, f1, f2, f3, &dv);
+    fac_f[idx] = (1.0f + half * dv) / denom;
+    gather_disp<ORDER, 1>(sd, d, i, j, k, b1, b2, b3, &dv);
+    fac_b[idx] = (1.0f + half * dv) / denom;
+  }
+}
+
+// ---- one semi-Lagrangian step: dst = interp(src, X) [* factor] --------------
+// state  : transport.py:130-133 (no factor)
+// adjoint: transport.py:154-155 (factor = adj_numer/adj_denom, backward trace)
+// jacobian: transport.py:194-195 (factor = jac_numer/jac_denom)
+template <int ORDER, bool SCALE>
+__global__ void __launch_bounds__(256) advect_kernel(const float* __restrict__ src, Dims d,
+                                                     const float* __restrict__ disp,
+                                                     const float* __restrict__ fac, float* __restrict__ dst,
+                                                     int* flag) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  SrcF32 s{{src, src, src}, 0};
+  float o;
+  gather_disp<ORDER, 1>(s, d, i, j, k, __ldg(disp + idx), __ldg(disp + N + idx), __ldg(disp + 2 * N + idx), &o);
+  if (SCALE) o *= __ldg(fac + idx);
+  dst[idx] = o;
+  flag_nonfinite(flag, o);
+}
+
+// ---- incremental state (transport.py:160-185) --------------------------------
+// s_j = -(vt . grad m^j);  u_0 = dt/2 s_0
+// m~_{j+1} = interp(u_j, X_f) + dt/2 s_{j+1};  u_{j+1} = m~_{j+1} + dt/2 s_{j+1}
+__device__ __forceinline__ float inc_source(const float* __restrict__ vt, const float* __restrict__ g, int64_t N,
+                                            int idx) {
+  return -(__ldg(vt + idx) * __ldg(g + idx) + __ldg(vt + N + idx) * __ldg(g + N + idx) +
+           __ldg(vt + 2 * N + idx) * __ldg(g + 2 * N + idx));
+}
+
+__global__ void __launch_bounds__(256) incstate_init_kernel(const float* __restrict__ vt,
+                                                            const float* __restrict__ g0, int64_t N, float half,
+                                                            float* __restrict__ u0) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  u0[idx] = half * inc_source(vt, g0, N, idx);
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(256) incstate_step_kernel(const float* __restrict__ u, Dims d,
+                                                            const float* __restrict__ disp,
+                                                            const float* __restrict__ vt,
+                                                            const float* __restrict__ gnext, float half,
+                                                            int last, float* __restrict__ out, int* flag) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  SrcF32 s{{u, u, u}, 0};
+  float o;
+  gather_disp<ORDER, 1>(s, d, i, j, k, __ldg(disp + idx), __ldg(disp + N + idx), __ldg(disp + 2 * N + idx), &o);
+  const float hs = half * inc_source(vt, gnext, N, idx);
+  float m = o + hs;
+  if (last == 0) m = m + hs;
+  else if (last == 2) m = -m;
+  out[idx] = m;
+  flag_nonfinite(flag, m);
+}
+
+// ---- trapezoidal body force (optim.py:162-171) --------------------------------
+// b = sum_j w_j lam^j grad m^j, w = dt/2 at j in {0,n}, dt otherwise; f64 accumulator
+__global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict__ lam,
+                                                         const float* __restrict__ gm, int nt, int64_t N,
+                                                         double dt, float* __restrict__ out) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int j = 0; j <= nt; ++j) {
+    const double w = (j == 0 || j == nt) ? 0.5 * dt : dt;
+    const float wl = (float)(w * (double)__ldg(lam + (int64_t)j * N + idx));
+    const float* g = gm + (int64_t)j * 3 * N;
+    a0 += (double)(wl * __ldg(g + idx));
+    a1 += (double)(wl * __ldg(g + N + idx));
+    a2 += (double)(wl * __ldg(g + 2 * N + idx));
+  }
+  out[idx] = (float)a0;
+  out[N + idx] = (float)a1;
+  out[2 * N + idx] = (float)a2;
+}
+
+// ---- label transport (synth.py:121-131) ---------------------------------------
+// First step gathers the indicator of `id` straight from the label map; the last
+// step thresholds at 0.5 and writes `id` (labels processed in ascending order, so
+// overlaps resolve to the larger id as in the reference).
+template <int ORDER, bool FROM_LABELS, bool TO_LABELS>
+__global__ void __launch_bounds__(256) label_step_kernel(const float* __restrict__ src,
+                                                         const int* __restrict__ lab_in, int id, Dims d,
+                                                         const float* __restrict__ disp,
+                                                         float* __restrict__ dst, int* __restrict__ lab_out) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  float o;
+  const float d1 = __ldg(disp + idx), d2 = __ldg(disp + N + idx), d3 = __ldg(disp + 2 * N + idx);
+  if (FROM_LABELS) {
+    SrcLabel s{lab_in, id};
+    gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
+  } else {
+    SrcF32 s{{src, src, src}, 0};
+    gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
+  }
+  if (TO_LABELS) {
+    if (o >= 0.5f) lab_out[idx] = id;
+  } else {
+    dst[idx] = o;
+  }
+}
+
+// ---- displacement -> absolute points in radians (Characteristics.points) ----
+__global__ void disp_to_points_kernel(const float* __restrict__ disp, Dims d, double* __restrict__ pts) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int ijk[3];
+  voxel_ijk(idx, d, ijk[0], ijk[1], ijk[2]);
+  const int n[3] = {d.n1, d.n2, d.n3};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double q = (double)ijk[a] - (double)disp[a * N + idx];
+    double h = kTwoPi / n[a];
+    double x = q * h;
+    x = fmod(x, kTwoPi);
+    if (x < 0) x += kTwoPi;
+    pts[a * N + idx] = x;
+  }
+}
+
+}  // namespace vr
+
+using namespace vr;
+
+#define VR_DISPATCH_ORDER(order, ...)                     \
+  if ((order) == 1) {                                     \
+    constexpr int ORD = ORDER_LINEAR;                     \
+    __VA_ARGS__;                                          \
+  } else if ((order) == 3) {                              \
+    constexpr int ORD = ORDER_CUBIC;                      \
+    __VA_ARGS__;                                          \
+  } else {                                                \
+    return VR_ERR_ARG;                                    \
+  }
+
+extern "C" {
+
+int vr_interp_points(const float* src, const int64_t dims[3], const void* pts, int pts_is_f64, int64_t npts,
+                     int order, float* out, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (npts < 0 || !src || !out || (!pts && npts)) return VR_ERR_ARG;
+  if (npts == 0) return VR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double h1 = kTwoPi / d.n1, h2 = kTwoPi / d.n2, h3 = kTwoPi / d.n3;
+  unsigned g = grid_for(npts, 256);
+  VR_DISPATCH_ORDER(order, {
+    if (pts_is_f64)
+      interp_points_kernel<ORD, double><<<g, 256, 0, s>>>(src, d, (const double*)pts, npts, h1, h2, h3, out);
+    else
+      interp_points_kernel<ORD, float><<<g, 256, 0, s>>>(src, d, (const float*)pts, npts, h1, h2, h3, out);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, float* disp_fwd, float* disp_bwd,
+                 const float* div, float* fac_jac, float* fac_adj, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!v || !disp_fwd || !disp_bwd || !(dt > 0)) return VR_ERR_ARG;
+  const bool factors = div != nullptr;
+  if (factors && (!fac_jac || !fac_adj)) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const float ih1 = (float)(d.n1 / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
+  unsigned g = grid_for(d.n(), 256);
+  VR_DISPATCH_ORDER(order, {
+    if (factors)
+      trace_kernel<ORD, true><<<g, 256, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div, fac_jac,
+                                                fac_adj);
+    else
+      trace_kernel<ORD, false><<<g, 256, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, nullptr,
+                                                 nullptr, nullptr);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_advect(const float* src, const int64_t dims[3], const float* disp, const float* factor, int order,
+              float* dst, int* nonfinite_flag, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!src || !disp || !dst || src == dst) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = grid_for(d.n(), 256);
+  VR_DISPATCH_ORDER(order, {
+    if (factor)
+      advect_kernel<ORD, true><<<g, 256, 0, s>>>(src, d, disp, factor, dst, nonfinite_flag);
+    else
+      advect_kernel<ORD, false><<<g, 256, 0, s>>>(src, d, disp, nullptr, dst, nonfinite_flag);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3], double dt, float* u0,
+                     void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!vt || !gradm0 || !u0) return VR_ERR_ARG;
+  incstate_init_kernel<<<grid_for(d.n(), 256), 256, 0, (cudaStream_t)stream>>>(vt, gradm0, d.n(),
+                                                                               (float)(0.5 * dt), u0);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fwd, const float* vt,
+                     const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
+                     void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = grid_for(d.n(), 256);
+  VR_DISPATCH_ORDER(order, {
+    incstate_step_kernel<ORD><<<g, 256, 0, s>>>(u, d, disp_fwd, vt, gradm_next, (float)(0.5 * dt), last, out,
+                                                nonfinite_flag);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
+                  float* out, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!lam_series || !gradm_series || !out || n_t < 1) return VR_ERR_ARG;
+  body_force_kernel<<<grid_for(d.n(), 256), 256, 0, (cudaStream_t)stream>>>(lam_series, gradm_series, n_t, d.n(),
+                                                                            dt, out);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_label_step(const float* src, const int* labels_in, int label_id, const int64_t dims[3], const float* disp,
+                  int order, float* dst, int* labels_out, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!disp || (!src && !labels_in) || (!dst && !labels_out)) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = grid_for(d.n(), 256);
+  const bool from_l = labels_in != nullptr, to_l = labels_out != nullptr;
+  VR_DISPATCH_ORDER(order, {
+    if (from_l && to_l)
+      label_step_kernel<ORD, true, true><<<g, 256, 0, s>>>(nullptr, labels_in, label_id, d, disp, nullptr,
+                                                           labels_out);
+    else if (from_l)
+      label_step_kernel<ORD, true, false><<<g, 256, 0, s>>>(nullptr, labels_in, label_id, d, disp, dst, nullptr);
+    else if (to_l)
+      label_step_kernel<ORD, false, true><<<g, 256, 0, s>>>(src, nullptr, label_id, d, disp, nullptr, labels_out);
+    else
+      label_step_kernel<ORD, false, false><<<g, 256, 0, s>>>(src, nullptr, label_id, d, disp, dst, nullptr);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_disp_to_points(const float* disp, const int64_t dims[3], double* pts, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!disp || !pts) return VR_ERR_ARG;
+  disp_to_points_kernel<<<grid_for(d.n(), 256), 256, 0, (cudaStream_t)stream>>>(disp, d, pts);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+"""Differential and spectral regularization operators (drop-in for
+/root/reference/pkg/src/velreg/diffops.py).
+
+FD8 gradient / divergence run the fp32 stencil kernel (bit-identical to the
+reference's numpy evaluation for float32 input).  A, its shifted inverse, the
+Leray blend K and the H1 energy run on the hand-written FFT engine
+(csrc/spectral.cu); `SpectralWorkspace` owns its plan (device buffers and
+twiddle tables) and, like the reference's, must not be shared by concurrent
+callers.
+"""
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+
+import ctypes as C
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import GridError
+from .grid import Grid, ScalarField, VectorField, TWO_PI
+
+FD8_COEFFS = (4.0 / 5.0, -1.0 / 5.0, 4.0 / 105.0, -1.0 / 280.0)   # diffops.py:20
+FD8_MIN_DIM = 9
+
+
+def _destroy_plan(handle):
+    lib = _lib.load_library()
+    lib.vr_spec_plan_destroy(handle)
+
+
+class SpectralWorkspace:
+    """Plan + scratch spectra for one grid (diffops.py:24-55).  The wavenumber
+    tables of the reference are exposed lazily as host arrays for inspection;
+    the device kernels regenerate wavenumbers from indices."""
+
+    def __init__(self, grid: Grid):
+        self.grid = grid
+        lib = _lib.lib()
+        handle = C.c_void_p()
+        _lib.check(lib.vr_spec_plan_create(_lib.dims_arg(grid.dims), C.byref(handle)), "vr_spec_plan_create")
+        self._plan = handle
+        self._finalizer = weakref.finalize(self, _destroy_plan, handle)
+        self.device = torch.cuda.current_device()
+
+    @property
+    def plan(self):
+        return self._plan
+
+    # host-side views of the reference's tables (diffops.py:34-49)
+    @property
+    def k(self):
+        n1, n2, n3 = self.grid.dims
+        return ((np.fft.fftfreq(n1) * n1).reshape(n1, 1, 1), (np.fft.fftfreq(n2) * n2).reshape(1, n2, 1),
+                np.arange(n3 // 2 + 1, dtype=np.float64).reshape(1, 1, n3 // 2 + 1))
+
+    @property
+    def ksq(self):
+        k1, k2, k3 = self.k
+        return k1 ** 2 + k2 ** 2 + k3 ** 2
+
+    @property
+    def mode_multiplicity(self):
+        n3 = self.grid.dims[2]
+        mult = np.full(self.ksq.shape, 2.0)
+        mult[:, :, 0] = 1.0
+        if n3 % 2 == 0:
+            mult[:, :, -1] = 1.0
+        return mult
+
+    def apply(self, kind: int, x: torch.Tensor, out: torch.Tensor | None = None, add: torch.Tensor | None = None,
+              beta_v: float = 0.0, beta_w: float = 0.0, shift: float = 0.0, sigma: float = 0.0,
+              alpha: float = 1.0) -> torch.Tensor:
+        ncomp = 3 if x.dim() == 4 else 1
+        if out is None:
+            out = torch.empty_like(x)
+        rc = _lib.lib().vr_spec_apply(self._plan, int(kind), x.data_ptr(), ncomp, float(beta_v), float(beta_w),
+                                      float(shift), float(sigma), float(alpha), _lib.ptr(add), out.data_ptr(),
+                                      _lib.stream())
+        _lib.check(rc, "vr_spec_apply")
+        return out
+
+    def h1_energy(self, f: torch.Tensor) -> float:
+        out = _lib.out_buf(1)
+        _lib.check(_lib.lib().vr_h1_energy(self._plan, f.data_ptr(), out.data_ptr(), _lib.stream()),
+                   "vr_h1_energy")
+        return float(out.cpu()[0])
+
+
+_ws_cache: dict = {}
+
+
+def workspace_for(grid: Grid) -> SpectralWorkspace:
+    key = (grid.dims, torch.cuda.current_device())
+    ws = _ws_cache.get(key)
+    if ws is None:
+        ws = SpectralWorkspace(grid)
+        _ws_cache[key] = ws
+    return ws
+
+
+@dataclass
+class RegOperators:
+    """Regularization weights plus the spectral workspace they act through
+    (diffops.py:58-75)."""
+
+    beta_v: float
+    beta_w: float
+    workspace: SpectralWorkspace = None
+
+    def __post_init__(self):
+        if not self.beta_v > 0:
+            raise ValueError(f"beta_v must be positive, got {self.beta_v}")
+        if self.beta_w < 0:
+            raise ValueError(f"beta_w must be non-negative, got {self.beta_w}")
+
+    @classmethod
+    def for_grid(cls, grid: Grid, beta_v: float, beta_w: float) -> "RegOperators":
+        return cls(beta_v, beta_w, workspace_for(grid))
+
+
+def _require_fd8(grid: Grid) -> None:
+    if min(grid.dims) < FD8_MIN_DIM:
+        raise GridError(f"8th-order stencil needs dims >= {FD8_MIN_DIM}, got {grid.dims}")
+
+
+# ---- FD8 (diffops.py:84-105) -------------------------------------------------
+def fd8_gradient_t(f: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    dims = tuple(f.shape[-3:])
+    if out is None:
+        out = torch.empty((3,) + dims, dtype=torch.float32, device=f.device)
+    _lib.check(_lib.lib().vr_fd8_grad(f.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
+               "vr_fd8_grad")
+    return out
+
+
+def fd8_divergence_t(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    dims = tuple(v.shape[-3:])
+    if out is None:
+        out = torch.empty(dims, dtype=torch.float32, device=v.device)
+    _lib.check(_lib.lib().vr_fd8_div(v.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
+               "vr_fd8_div")
+    return out
+
+
+def fd8_gradient(f: ScalarField) -> VectorField:
+    _require_fd8(f.grid)
+    return VectorField(f.grid, fd8_gradient_t(f.values))
+
+
+def fd8_divergence(v: VectorField) -> ScalarField:
+    _require_fd8(v.grid)
+    return ScalarField(v.grid, fd8_divergence_t(v.data))
+
+
+# ---- spectral operators (diffops.py:108-154) -------------------------------------
+def apply_A(v: VectorField, ops: RegOperators) -> VectorField:
+    """Negative vector Laplacian (symbol |k|^2); kills constants."""
+    return VectorField(v.grid, ops.workspace.apply(_lib.SPEC_A, v.data))
+
+
+def apply_inv_shifted_A(v: VectorField, ops: RegOperators, shift: float) -> VectorField:
+    """Spectral inverse of (beta_v*A + shift*I); preconditioner support."""
+    if not shift > 0:
+        raise ValueError(f"shift must be positive, got {shift}")
+    return VectorField(v.grid, ops.workspace.apply(_lib.SPEC_INVSHIFT, v.data, beta_v=ops.beta_v, shift=shift))
+
+
+def apply_K(g: VectorField, ops: RegOperators) -> VectorField:
+    """Blend toward the Leray projection (diffops.py:129-146); beta_w = 0 is the
+    identity (a copy, as in the reference)."""
+    if ops.beta_w == 0.0:
+        return g.copy()
+    return VectorField(g.grid, ops.workspace.apply(_lib.SPEC_K, g.data, beta_v=ops.beta_v, beta_w=ops.beta_w))
+
+
+def h1_energy(f: ScalarField, ws: SpectralWorkspace) -> float:
+    """Spectral H1 norm squared: integral of f^2 + |grad f|^2 over the box."""
+    return ws.h1_energy(f.values)
+
+
+# ---- north-star extras without a reference counterpart (flags default off) -------
+def gaussian_smooth(v, ws: SpectralWorkspace, sigma: float):
+    """Spectral Gaussian smoothing exp(-sigma^2 |k|^2 / 2) (sigma in voxels of the
+    unit-wavenumber lattice); pinned analytically by eigenfunction tests."""
+    data = v.data if isinstance(v, VectorField) else v.values
+    out = ws.apply(_lib.SPEC_GAUSS, data, sigma=sigma)
+    return VectorField(v.grid, out) if isinstance(v, VectorField) else ScalarField(v.grid, out)
+
+
+def apply_A2(v: VectorField, ops: RegOperators) -> VectorField:
+    """H2-seminorm operator (bi-Laplacian, symbol |k|^4)."""
+    return VectorField(v.grid, ops.workspace.apply(_lib.SPEC_A2, v.data))
+
+
+def apply_inv_shifted_A2(v: VectorField, ops: RegOperators, shift: float) -> VectorField:
+    if not shift > 0:
+        raise ValueError(f"shift must be positive, got {shift}")
+    return VectorField(v.grid, ops.workspace.apply(_lib.SPEC_INVSHIFT2, v.data, beta_v=ops.beta_v, shift=shift))

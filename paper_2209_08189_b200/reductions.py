@@ -1,0 +1,87 @@
+"""Host wrappers of the deterministic f64 reductions and fused vector updates
+(csrc/reduce.cu).  Each reduction is one device pass plus a single-CTA fold;
+results come back to the host in one small copy (the only host sync points of
+the solver, matching where the reference needs a Python float)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _n(t: torch.Tensor) -> int:
+    return t.numel()
+
+
+def dots(pairs) -> np.ndarray:
+    """[sum(a*b) for a, b in pairs] (<= 4 pairs, same length) -> float64 array."""
+    lib = _lib.lib()
+    k = len(pairs)
+    assert 1 <= k <= 4
+    n = _n(pairs[0][0])
+    out = _lib.out_buf(k)
+    a = _lib.ptr_array([p[0] for p in pairs])
+    b = _lib.ptr_array([p[1] for p in pairs])
+    _lib.check(lib.vr_dots(k, a, b, n, _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()), "vr_dots")
+    return out.cpu().numpy()
+
+
+def dot(a: torch.Tensor, b: torch.Tensor) -> float:
+    return float(dots([(a, b)])[0])
+
+
+def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> np.ndarray:
+    lib = _lib.lib()
+    out = _lib.out_buf(2)
+    _lib.check(lib.vr_sqdiff(a.data_ptr(), b.data_ptr(), _lib.ptr(c), _n(a), _lib.scratch().data_ptr(),
+                             out.data_ptr(), _lib.stream()), "vr_sqdiff")
+    return out.cpu().numpy()
+
+
+def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
+    lib = _lib.lib()
+    out = _lib.out_buf(4)
+    _lib.check(lib.vr_minmax(a.data_ptr(), _lib.ptr(b), _n(a), _lib.scratch().data_ptr(), out.data_ptr(),
+                             _lib.stream()), "vr_minmax")
+    return out.cpu().numpy()
+
+
+def vecstats(v: torch.Tensor) -> tuple:
+    """(max_x |v(x)|^2, number of non-finite entries, number of non-zero entries)"""
+    lib = _lib.lib()
+    out = _lib.out_buf(4)
+    _lib.check(lib.vr_vecstats(v.data_ptr(), _n(v) // 3, _lib.scratch().data_ptr(), out.data_ptr(),
+                               _lib.stream()), "vr_vecstats")
+    o = out.cpu().numpy()
+    return float(o[1]), int(o[2]), int(o[3])
+
+
+def axpby(a: float, x: torch.Tensor, b: float = 0.0, y: torch.Tensor | None = None,
+          out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = a*x + b*y (f64 arithmetic, f32 storage)."""
+    if out is None:
+        out = torch.empty_like(x)
+    _lib.check(_lib.lib().vr_axpby(_n(x), float(a), x.data_ptr(), float(b), _lib.ptr(y), out.data_ptr(),
+                                   _lib.stream()), "vr_axpby")
+    return out
+
+
+def pcg_update(alpha: float, p: torch.Tensor, hp: torch.Tensor, x: torch.Tensor, r: torch.Tensor) -> None:
+    _lib.check(_lib.lib().vr_pcg_update(_n(x), float(alpha), p.data_ptr(), hp.data_ptr(), x.data_ptr(),
+                                        r.data_ptr(), _lib.stream()), "vr_pcg_update")
+
+
+def fill(out: torch.Tensor, value: float) -> torch.Tensor:
+    _lib.check(_lib.lib().vr_fill(_n(out), float(value), out.data_ptr(), _lib.stream()), "vr_fill")
+    return out
+
+
+def label_histogram(l0: torch.Tensor, l1: torch.Tensor, max_id: int | None = None) -> np.ndarray:
+    """counts[id] = (|l0==id|, |l1==id|, |l0==id & l1==id|) as exact int64."""
+    if max_id is None:
+        max_id = int(max(int(l0.max()), int(l1.max()))) if l0.numel() else 0
+    counts = torch.empty(3 * (max_id + 1), dtype=torch.int64, device=l0.device)
+    _lib.check(_lib.lib().vr_label_counts(l0.data_ptr(), l1.data_ptr(), _n(l0), int(max_id), counts.data_ptr(),
+                                          _lib.stream()), "vr_label_counts")
+    return counts.cpu().numpy().reshape(max_id + 1, 3)

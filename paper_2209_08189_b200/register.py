@@ -1,0 +1,62 @@
+"""`register(m0, m1, params)` -- the north star's drop-in entry point.
+
+The reference has no single call for this; it is the composition used by its
+CLI and experiment driver: gauss_newton_register (optim.py:275) -> solve_state
+of the template (cli.py:134-141) -> relative_residual (optim.py:364) ->
+optional transport_labels + dice_averages (experiment.py:132-135).  Everything
+stays on the device; host <-> device traffic is the two input images (and
+label maps) in, and whatever the caller pulls out of the result.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .grid import Grid, LabelMap, ScalarField, VectorField
+from .metrics import DiceReport, dice_averages
+from .optim import RegistrationConfig, SolverDiagnostics, gauss_newton_solve
+from .synth import transport_labels
+
+
+@dataclass
+class RegistrationResult:
+    velocity: VectorField
+    deformed: ScalarField
+    relative_residual: float
+    diagnostics: SolverDiagnostics
+    dice: DiceReport | None = None
+    dice_pre: DiceReport | None = None
+
+    @property
+    def mismatch(self) -> float:
+        return self.relative_residual
+
+
+def _as_field(x, grid: Grid | None) -> ScalarField:
+    if isinstance(x, ScalarField):
+        return x
+    if grid is None:
+        grid = Grid(tuple(x.shape))
+    return ScalarField(grid, x)
+
+
+def register(m0, m1, params: RegistrationConfig | dict | None = None, labels0=None, labels1=None,
+             v0: VectorField | None = None, pre_dice: bool = False) -> RegistrationResult:
+    """Register template m0 to reference m1 (arrays, tensors or ScalarFields)."""
+    if params is None:
+        cfg = RegistrationConfig()
+    elif isinstance(params, dict):
+        cfg = RegistrationConfig(**params)
+    else:
+        cfg = params
+    m0 = _as_field(m0, None)
+    m1 = _as_field(m1, m0.grid)
+    v, diag, state = gauss_newton_solve(m0, m1, cfg, v0)
+    res = RegistrationResult(v, state.deformed, diag.relative_residual, diag)
+    if labels0 is not None and labels1 is not None:
+        l0 = labels0 if isinstance(labels0, LabelMap) else LabelMap(m0.grid, labels0)
+        l1 = labels1 if isinstance(labels1, LabelMap) else LabelMap(m0.grid, labels1)
+        moved = transport_labels(l0, v, cfg.transport(), state.transport_ops)
+        res.dice = dice_averages(moved, l1)
+        if pre_dice:
+            res.dice_pre = dice_averages(l0, l1)
+    return res

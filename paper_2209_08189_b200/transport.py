@@ -1,0 +1,271 @@
+"""Semi-Lagrangian transport solvers (drop-in for
+/root/reference/pkg/src/velreg/transport.py).
+
+One RK2 (Heun) characteristic trace per velocity iterate is shared by every
+solve (forward trace for state / incremental state / Jacobian, backward trace
+for the adjoint), with trapezoidal divergence source factors.  All sweeps run
+in HBM on the sm_100a kernels of csrc/transport.cu; the host only sequences the
+n_t steps and reads the non-finite flag where the reference checks
+(transport.py:57-59, 119-121).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .diffops import fd8_divergence_t, fd8_gradient_t
+from .errors import TransportError
+from .grid import Grid, ScalarField, VectorField, TWO_PI
+
+INTERP_ORDERS = ("linear", "cubic")
+
+
+@dataclass
+class TransportConfig:
+    n_t: int = 4
+    interp_order: str = "cubic"
+    direction: str = "forward"
+
+    def __post_init__(self):
+        if self.n_t < 1:
+            raise ValueError(f"n_t must be >= 1, got {self.n_t}")
+        if self.interp_order not in INTERP_ORDERS:
+            raise ValueError(f"interp_order must be in {INTERP_ORDERS}")
+        if self.direction not in ("forward", "backward"):
+            raise ValueError("direction must be 'forward' or 'backward'")
+
+    @property
+    def dt(self) -> float:
+        return 1.0 / self.n_t
+
+
+@dataclass
+class Characteristics:
+    """Departure points of every voxel, stored as index-unit displacements
+    (3, N1, N2, N3) float32; `.points` gives the reference's radians in
+    [0, 2*pi) (float64) on demand."""
+
+    grid: Grid
+    displacement: torch.Tensor
+    dt: float
+
+    @property
+    def points(self) -> torch.Tensor:
+        out = torch.empty((3,) + self.grid.dims, dtype=torch.float64, device=self.displacement.device)
+        _lib.check(_lib.lib().vr_disp_to_points(self.displacement.data_ptr(), _lib.dims_arg(self.grid.dims),
+                                                out.data_ptr(), _lib.stream()), "vr_disp_to_points")
+        return out
+
+
+def cfl_number(v: VectorField, dt: float) -> float:
+    """transport.py:53-54"""
+    return dt * v.max_pointwise_norm() / min(v.grid.spacing)
+
+
+def _check_finite_velocity(v: VectorField) -> None:
+    if v.stats()[1] > 0:
+        raise TransportError("velocity field contains non-finite values")
+
+
+def _order(order: str) -> int:
+    if order not in INTERP_ORDERS:
+        raise ValueError(f"interpolation order must be one of {INTERP_ORDERS}, got {order!r}")
+    return _lib.ORDER[order]
+
+
+def _trace(v: torch.Tensor, dims, dt: float, order: str, div: torch.Tensor | None = None):
+    disp_f = torch.empty_like(v)
+    disp_b = torch.empty_like(v)
+    fac_j = fac_a = None
+    if div is not None:
+        fac_j = torch.empty_like(div)
+        fac_a = torch.empty_like(div)
+    rc = _lib.lib().vr_trace_rk2(v.data_ptr(), _lib.dims_arg(dims), float(dt), _order(order), disp_f.data_ptr(),
+                                 disp_b.data_ptr(), _lib.ptr(div), _lib.ptr(fac_j), _lib.ptr(fac_a), _lib.stream())
+    _lib.check(rc, "vr_trace_rk2")
+    return disp_f, disp_b, fac_j, fac_a
+
+
+def trace_characteristics(v: VectorField, dt: float, order: str = "cubic") -> Characteristics:
+    """RK2 (Heun) backward trace: x* = x - dt*v(x), X = x - dt/2*(v(x) + v(x*))
+    (transport.py:66-76)."""
+    if not dt > 0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    _check_finite_velocity(v)
+    disp_f, _, _, _ = _trace(v.data, v.grid.dims, dt, order)
+    return Characteristics(v.grid, disp_f, dt)
+
+
+def advect(values: torch.Tensor, disp: torch.Tensor, order: str, factor: torch.Tensor | None = None,
+           out: torch.Tensor | None = None, flag: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(values.shape, dtype=torch.float32, device=values.device)
+    rc = _lib.lib().vr_advect(values.data_ptr(), _lib.dims_arg(values.shape[-3:]), disp.data_ptr(),
+                              _lib.ptr(factor), _order(order), out.data_ptr(), _lib.ptr(flag), _lib.stream())
+    _lib.check(rc, "vr_advect")
+    return out
+
+
+def interpolate(f: ScalarField, chars: Characteristics, order: str) -> ScalarField:
+    if f.grid != chars.grid:
+        raise TransportError("field and characteristics grids differ")
+    return ScalarField(f.grid, advect(f.values, chars.displacement, order))
+
+
+class TransportOperators:
+    """Shared per-velocity data for all transport solves at one iterate
+    (transport.py:89-116): both characteristic traces, the FD8 divergence and
+    the trapezoidal source factors, built by ONE fused trace kernel after the
+    divergence kernel.  The factors are stored as ratios
+    jac_factor = jac_numer / jac_denom and adj_factor = adj_numer / adj_denom."""
+
+    def __init__(self, v: VectorField, cfg: TransportConfig):
+        _check_finite_velocity(v)
+        self.v = v
+        self.cfg = cfg
+        self.grid = v.grid
+        self.div = fd8_divergence_t(v.data)
+        disp_f, disp_b, self.jac_factor, self.adj_factor = _trace(v.data, v.grid.dims, cfg.dt, cfg.interp_order,
+                                                                  self.div)
+        self.forward = Characteristics(v.grid, disp_f, cfg.dt)
+        self.backward = Characteristics(v.grid, disp_b, cfg.dt)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=v.data.device)
+
+    def advect_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
+        return advect(values, self.forward.displacement, self.cfg.interp_order, out=out, flag=flag)
+
+    def advect_back_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
+        return advect(values, self.backward.displacement, self.cfg.interp_order, out=out, flag=flag)
+
+    # non-finite guard (transport.py:119-121) read back at the reference's check points
+    def arm(self) -> torch.Tensor:
+        self.flag.zero_()
+        return self.flag
+
+    def raise_if_flagged(self, what: str) -> None:
+        if int(self.flag.item()) != 0:
+            raise TransportError(f"{what} produced non-finite values")
+
+
+def _ops_for(v: VectorField, cfg: TransportConfig, ops) -> TransportOperators:
+    return ops or TransportOperators(v, cfg)
+
+
+def solve_state_series(m0: ScalarField, v: VectorField, cfg: TransportConfig,
+                       ops: TransportOperators = None) -> torch.Tensor:
+    """All n_t + 1 snapshots of the transported template, shape (n_t+1,) + dims
+    (transport.py:124-135)."""
+    if m0.grid != v.grid:
+        raise TransportError("template and velocity grids differ")
+    ops = _ops_for(v, cfg, ops)
+    series = torch.empty((cfg.n_t + 1,) + m0.grid.dims, dtype=torch.float32, device=m0.values.device)
+    series[0].copy_(m0.values)
+    flag = ops.arm()
+    for j in range(cfg.n_t):
+        ops.advect_step(series[j], out=series[j + 1], flag=flag if j == cfg.n_t - 1 else None)
+    ops.raise_if_flagged("state solve")
+    return series
+
+
+def solve_state(m0: ScalarField, v: VectorField, cfg: TransportConfig,
+                ops: TransportOperators = None) -> ScalarField:
+    """Deformed template m(., 1) after n_t semi-Lagrangian steps (transport.py:138-142);
+    ping-pongs two buffers instead of keeping the series."""
+    if m0.grid != v.grid:
+        raise TransportError("template and velocity grids differ")
+    ops = _ops_for(v, cfg, ops)
+    a = m0.values
+    bufs = [torch.empty_like(a), torch.empty_like(a)]
+    flag = ops.arm()
+    for j in range(cfg.n_t):
+        dst = bufs[j % 2]
+        ops.advect_step(a, out=dst, flag=flag if j == cfg.n_t - 1 else None)
+        a = dst
+    ops.raise_if_flagged("state solve")
+    return ScalarField(m0.grid, a)
+
+
+def solve_adjoint(final_lambda: ScalarField, v: VectorField, cfg: TransportConfig,
+                  ops: TransportOperators = None) -> torch.Tensor:
+    """Backward continuity solve; all snapshots indexed by forward time
+    (transport.py:145-157)."""
+    if final_lambda.grid != v.grid:
+        raise TransportError("adjoint final condition and velocity grids differ")
+    ops = _ops_for(v, cfg, ops)
+    series = torch.empty((cfg.n_t + 1,) + v.grid.dims, dtype=torch.float32, device=v.data.device)
+    series[cfg.n_t].copy_(final_lambda.values)
+    _adjoint_sweep(series, ops, cfg)
+    return series
+
+
+def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: TransportConfig) -> None:
+    flag = ops.arm()
+    for j in range(cfg.n_t - 1, -1, -1):
+        advect(series[j + 1], ops.backward.displacement, cfg.interp_order, factor=ops.adj_factor, out=series[j],
+               flag=flag if j == 0 else None)
+    ops.raise_if_flagged("adjoint solve")
+
+
+def gradient_series(m_series: torch.Tensor) -> torch.Tensor:
+    """FD8 gradient of every snapshot, (n_t+1, 3) + dims (optim.py:127-135)."""
+    out = torch.empty((m_series.shape[0], 3) + tuple(m_series.shape[1:]), dtype=torch.float32,
+                      device=m_series.device)
+    for j in range(m_series.shape[0]):
+        fd8_gradient_t(m_series[j], out=out[j])
+    return out
+
+
+def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOperators, cfg: TransportConfig,
+                 last_mode: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    lib = _lib.lib()
+    dims = ops.grid.dims
+    d = _lib.dims_arg(dims)
+    st = _lib.stream()
+    u = torch.empty(dims, dtype=torch.float32, device=vt.device)
+    _lib.check(lib.vr_incstate_init(vt.data_ptr(), grad_m_series[0].data_ptr(), d, float(cfg.dt), u.data_ptr(), st),
+               "vr_incstate_init")
+    other = torch.empty_like(u)
+    flag = ops.arm()
+    order = _order(cfg.interp_order)
+    for j in range(cfg.n_t):
+        last = j == cfg.n_t - 1
+        dst = out if (last and out is not None) else other
+        rc = lib.vr_incstate_step(u.data_ptr(), d, ops.forward.displacement.data_ptr(), vt.data_ptr(),
+                                  grad_m_series[j + 1].data_ptr(), float(cfg.dt), order, last_mode if last else 0,
+                                  dst.data_ptr(), _lib.ptr(flag) if last else None, st)
+        _lib.check(rc, "vr_incstate_step")
+        if not last:
+            u, other = dst, u
+        else:
+            u = dst
+    ops.raise_if_flagged("incremental state solve")
+    return u
+
+
+def solve_incremental_state(m_series: torch.Tensor, v: VectorField, v_tilde: VectorField,
+                            cfg: TransportConfig, ops: TransportOperators = None,
+                            grad_m_series: torch.Tensor = None) -> ScalarField:
+    """Linearized state dm~/dt + v.grad(m~) = -v~.grad(m), m~(0) = 0 (transport.py:160-185)."""
+    ops = _ops_for(v, cfg, ops)
+    if grad_m_series is None:
+        grad_m_series = gradient_series(torch.as_tensor(m_series).to(v.data.device, torch.float32))
+    return ScalarField(v.grid, _incremental(grad_m_series, v_tilde.data, ops, cfg, 1))
+
+
+def jacobian_determinant(v: VectorField, cfg: TransportConfig, ops: TransportOperators = None) -> ScalarField:
+    """det of the deformation gradient at t = 1 via dJ/dt + v.grad(J) = J div(v),
+    J(0) = 1 (transport.py:188-197)."""
+    ops = _ops_for(v, cfg, ops)
+    cur = torch.empty(v.grid.dims, dtype=torch.float32, device=v.data.device)
+    from .reductions import fill
+    fill(cur, 1.0)
+    other = torch.empty_like(cur)
+    flag = ops.arm()
+    for j in range(cfg.n_t):
+        advect(cur, ops.forward.displacement, cfg.interp_order, factor=ops.jac_factor, out=other,
+               flag=flag if j == cfg.n_t - 1 else None)
+        cur, other = other, cur
+    ops.raise_if_flagged("Jacobian-determinant solve")
+    return ScalarField(v.grid, cur)

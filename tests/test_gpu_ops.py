@@ -1,0 +1,185 @@
+"""Per-operator parity of the CUDA path against the reference.
+
+Inputs are the float32 arrays of the golden fixture (tests/golden/ops_16x20x24,
+made by the LIVE reference); larger sizes compare against the CPU oracle
+(pinned to the same fixtures by test_oracle_golden.py) on identical float32
+inputs.  Tolerance: the north star's <= 1e-5 relative L2 per operator; FD8 is
+bit-exact for float32 input.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2209_08189_b200 as P
+    assert torch.cuda.is_available()
+    return P
+
+
+def _grid(P, fx):
+    return P.make_grid(tuple(int(n) for n in fx["dims"]))
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def test_interpolate_values(P, ops_fx):
+    g = _grid(P, ops_fx)
+    for order in ("linear", "cubic"):
+        for src in ("smooth", "rand"):
+            vals = ops_fx[f"f_{src}"]
+            got = P.interpolate_values(vals, ops_fx[f"trace_fwd_{order}"].astype(np.float64), order, g.spacing)
+            assert rel_l2(_np(got), ops_fx[f"interp_{order}_{src}_trace"]) < TOL
+            got = P.interpolate_values(vals, ops_fx["pts_rand"], order, g.spacing)   # f32 points, out of box
+            assert rel_l2(_np(got), ops_fx[f"interp_{order}_{src}_rand"]) < TOL
+
+
+def test_trace_characteristics(P, ops_fx):
+    g = _grid(P, ops_fx)
+    v = P.VectorField(g, ops_fx["v"])
+    for order in ("linear", "cubic"):
+        for sign, key in ((1, "fwd"), (-1, "bwd")):
+            vv = v if sign > 0 else P.VectorField(g, -ops_fx["v"])
+            pts = _np(P.trace_characteristics(vv, 0.25, order).points)
+            d = np.abs(pts - ops_fx[f"trace_{key}_{order}"])
+            d = np.minimum(d, 2 * math.pi - d)   # periodic
+            assert d.max() < 1e-5
+
+
+def test_fd8_bit_exact(P, ops_fx):
+    g = _grid(P, ops_fx)
+    got = _np(P.fd8_gradient(P.ScalarField(g, ops_fx["f_rand"])).data)
+    np.testing.assert_array_equal(got, ops_fx["fd8_grad_f32"])
+    got = _np(P.fd8_divergence(P.VectorField(g, ops_fx["w"])).values)
+    np.testing.assert_array_equal(got, ops_fx["fd8_div_f32"])
+    assert rel_l2(got, ops_fx["fd8_div"]) < TOL
+
+
+def test_fd8_requires_nine(P):
+    g = P.make_grid((8, 16, 16))
+    with pytest.raises(P.GridError):
+        P.fd8_gradient(P.ScalarField.zeros(g))
+
+
+def test_spectral_operators(P, ops_fx):
+    g = _grid(P, ops_fx)
+    ops = P.RegOperators.for_grid(g, 1e-2, 1e-4)
+    v = P.VectorField(g, ops_fx["v"])
+    w = P.VectorField(g, ops_fx["w"])
+    assert rel_l2(_np(P.apply_A(v, ops).data), ops_fx["apply_A_v"]) < TOL
+    assert rel_l2(_np(P.apply_A(w, ops).data), ops_fx["apply_A_w"]) < TOL
+    assert rel_l2(_np(P.apply_inv_shifted_A(w, ops, 1.0).data), ops_fx["inv_shifted_A_w_1"]) < TOL
+    assert rel_l2(_np(P.apply_inv_shifted_A(w, ops, 0.37).data), ops_fx["inv_shifted_A_w_037"]) < TOL
+    assert rel_l2(_np(P.apply_K(w, ops).data), ops_fx["apply_K_w"]) < TOL
+    assert rel_l2(_np(P.apply_K(v, ops).data), ops_fx["apply_K_v"]) < TOL
+    ops3 = P.RegOperators.for_grid(g, 1e-2, 3.0)
+    assert rel_l2(_np(P.apply_K(w, ops3).data), ops_fx["apply_K_w_bw3"]) < TOL
+    ops0 = P.RegOperators.for_grid(g, 1e-2, 0.0)
+    assert torch.equal(P.apply_K(w, ops0).data, w.data)   # beta_w = 0 -> identity copy
+    div = P.fd8_divergence(v)
+    assert abs(P.h1_energy(div, ops.workspace) / float(ops_fx["h1_energy_divv"]) - 1) < TOL
+    fr = P.ScalarField(g, ops_fx["f_rand"])
+    assert abs(P.h1_energy(fr, ops.workspace) / float(ops_fx["h1_energy_frand"]) - 1) < TOL
+
+
+def test_transport_sweeps(P, ops_fx):
+    g = _grid(P, ops_fx)
+    v = P.VectorField(g, ops_fx["v"])
+    vt = P.VectorField(g, ops_fx["vt"])
+    f = P.ScalarField(g, ops_fx["f_smooth"])
+    lam = P.ScalarField(g, ops_fx["f_rand"] - 0.5)
+    for order in ("linear", "cubic"):
+        cfg = P.TransportConfig(4, order)
+        tops = P.TransportOperators(v, cfg)
+        jac = ops_fx[f"jac_numer_{order}"].astype(np.float64) / ops_fx[f"jac_denom_{order}"]
+        adj = ops_fx[f"adj_numer_{order}"].astype(np.float64) / ops_fx[f"adj_denom_{order}"]
+        assert rel_l2(_np(tops.jac_factor), jac) < TOL
+        assert rel_l2(_np(tops.adj_factor), adj) < TOL
+        series = P.solve_state_series(f, v, cfg, tops)
+        assert rel_l2(_np(series), ops_fx[f"state_series_{order}"]) < TOL
+        assert rel_l2(_np(P.solve_state(f, v, cfg, tops).values), ops_fx[f"state_series_{order}"][-1]) < TOL
+        assert rel_l2(_np(P.solve_adjoint(lam, v, cfg, tops)), ops_fx[f"adjoint_series_{order}"]) < TOL
+        inc = P.solve_incremental_state(series, v, vt, cfg, tops)
+        assert rel_l2(_np(inc.values), ops_fx[f"incstate_{order}"]) < TOL
+        assert rel_l2(_np(P.jacobian_determinant(v, cfg, tops).values), ops_fx[f"jacobian_{order}"]) < TOL
+
+
+def test_objective_gradient_matvec(P, ops_fx):
+    g = _grid(P, ops_fx)
+    v = P.VectorField(g, 0.5 * ops_fx["v"].astype(np.float64))
+    w = P.VectorField(g, ops_fx["w"])
+    for order in ("cubic", "linear"):
+        m0 = P.ScalarField(g, ops_fx[f"obj_m0_{order}"])
+        m1 = P.ScalarField(g, ops_fx[f"obj_m1_{order}"])
+        for bw in (0.0, 1e-4):
+            tag = f"{order}_bw{bw:g}"
+            cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=bw, n_t=4, interp_order=order)
+            st = P.ObjectiveState(m0, m1, v, cfg, P.RegOperators.for_grid(g, 1e-2, bw))
+            assert abs(st.objective / float(ops_fx[f"objective_{tag}"]) - 1) < TOL
+            assert rel_l2(_np(st.deformed.values), ops_fx[f"deformed_{tag}"]) < TOL
+            assert rel_l2(_np(st.gradient.data), ops_fx[f"gradient_{tag}"]) < TOL
+            assert rel_l2(_np(P.hessian_matvec(w, st).data), ops_fx[f"matvec_{tag}"]) < TOL
+
+
+def test_labels_and_dice(P, ops_fx):
+    g = _grid(P, ops_fx)
+    v = P.VectorField(g, ops_fx["v"])
+    lab0 = P.LabelMap(g, ops_fx["labels0"])
+    for order in ("cubic", "linear"):
+        moved = P.transport_labels(lab0, v, P.TransportConfig(4, order))
+        ref = ops_fx[f"labels_moved_{order}"]
+        assert int((_np(moved.labels) != ref).sum()) == 0
+        rep = P.dice_averages(moved, lab0)
+        np.testing.assert_allclose([rep.d_a, rep.d_vw, rep.d_ivw], ops_fx[f"dice_avgs_{order}"], rtol=1e-6)
+        assert rep.label_ids == [int(i) for i in ops_fx[f"dice_ids_{order}"]]
+
+
+def test_restrict(P, ops_fx):
+    g = _grid(P, ops_fx)
+    got = P.restrict(P.ScalarField(g, ops_fx["f_rand"]), 2)
+    np.testing.assert_array_equal(_np(got.values), ops_fx["restrict2_f"])
+
+
+def test_prolong_spectral(P, ops_fx):
+    g = _grid(P, ops_fx)
+    coarse = P.make_grid(tuple(n // 2 for n in g.dims))
+    got = P.prolong_spectral(P.VectorField(coarse, ops_fx["prolong_in"]), g)
+    assert rel_l2(_np(got.data), ops_fx["prolong_out"]) < TOL
+
+
+# ---- larger grids against the oracle (identical float32 inputs) ----------------
+@pytest.mark.parametrize("n", [64, 96])
+def test_ops_vs_oracle(P, n):
+    from oracle import velreg_oracle as O
+    dims = (n, n, n)
+    g = P.make_grid(dims)
+    rng = np.random.default_rng(n)
+    v = (0.2 * O.velocity(2, dims)).astype(np.float32)
+    f = rng.random(dims).astype(np.float32)
+    w = rng.standard_normal((3,) + dims).astype(np.float32)
+    v64 = v.astype(np.float64)
+    for order in ("linear", "cubic"):
+        tr = O.Transport(v64, 4, order)
+        tops = P.TransportOperators(P.VectorField(g, v), P.TransportConfig(4, order))
+        fs = P.ScalarField(g, f)
+        got = _np(P.solve_state(fs, tops.v, tops.cfg, tops).values)
+        assert rel_l2(got, tr.state_series(f.astype(np.float64))[-1]) < TOL
+        assert rel_l2(_np(tops.jac_factor), tr.jac_numer / tr.jac_denom) < TOL
+    ops = P.RegOperators.for_grid(g, 1e-2, 1e-4)
+    W = P.VectorField(g, w)
+    assert rel_l2(_np(P.apply_A(W, ops).data), O.op_A(w.astype(np.float64))) < TOL
+    assert rel_l2(_np(P.apply_K(W, ops).data), O.op_K(w.astype(np.float64), 1e-2, 1e-4)) < TOL
+    assert rel_l2(_np(P.apply_inv_shifted_A(W, ops, 1.0).data),
+                  O.op_inv_shifted(w.astype(np.float64), 1e-2, 1.0)) < TOL
+    np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), O.grad(f))
