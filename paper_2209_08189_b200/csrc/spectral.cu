@@ -26,6 +26,8 @@
 // (e.g. the CLARITY sizes 2816 = 2^8*11, 3016 = 2^3*13*29, 1162 = 2*7*83).
 #include <vector>
 #include <new>
+#include <type_traits>
+#include <algorithm>
 #include "common.cuh"
 #include "../../include/velreg_b200.h"
 
@@ -483,19 +485,24 @@ __global__ void finalize_sum_kernel(const double* __restrict__ partials, int n, 
 
 }  // namespace vr
 
+#include "spectral_fast.cuh"
+
 using namespace vr;
+
 
 struct vr_spec_plan {
   Dims d;
   int n3h;
   int64_t nspec;  // n1*n2*n3h
+  bool fast;      // n1, n2, n3/2 powers of two in [8, 2048]
   RadixPlan rp1, rp2, rp3;
-  double2 *tw1, *tw2, *tw3;
+  double2 *tw1, *tw2, *tw3, *tw3h;  // W_n1, W_n2, W_n3, W_{n3/2}
+  double2 *stw1, *stw2, *stw3h;     // fast path: per-stage tables (2L entries)
   double2* S;      // 3 * nspec (forward, f64)
   float2* T;       // 3 * nspec (inverse, f32)
   double* partials;
-  int RBz, RBzi, By, Byi, Bx1, Bx3;
-  size_t smz, smzi, smy, smyi, smx1, smx3;
+  int RBz, RBzi, Bx1, Bx3;
+  size_t smz, smzi, smx1, smx3;
   int device;
 };
 
@@ -507,6 +514,8 @@ int pow2_floor(int x) {
   return p;
 }
 
+bool is_pow2_in(int x, int lo, int hi) { return x >= lo && x <= hi && (x & (x - 1)) == 0; }
+
 int choose_lines(int L, int ncomp, size_t elem, size_t budget, int cap) {
   int B = (int)(budget / (2 * (size_t)ncomp * (L + 1) * elem));
   if (B < 1) B = 1;
@@ -517,7 +526,6 @@ int choose_lines(int L, int ncomp, size_t elem, size_t budget, int cap) {
 int upload_twiddles(int L, double2** out) {
   std::vector<double2> h(L);
   for (int m = 0; m < L; ++m) {
-    // e^{-2 pi i m / L}; reduce the angle to the first octant-friendly range
     double ang = -kTwoPi * (double)m / (double)L;
     h[m] = make_double2(cos(ang), sin(ang));
   }
@@ -526,7 +534,83 @@ int upload_twiddles(int L, double2** out) {
   return VR_OK;
 }
 
+// Per-stage twiddles of the fast Stockham engine: entry NS + k = W_{NS R}^k for
+// every stage (span NS > 1, radix R = min(8, L / NS)); stages are powers of 8
+// apart, so the ranges [NS, 2 NS) are disjoint and lanes read consecutive slots.
+int upload_stage_twiddles(int L, double2** out) {
+  std::vector<double2> h(2 * (size_t)L, make_double2(1.0, 0.0));
+  for (int ns = 8; ns < L; ns *= 8) {
+    const int R = std::min(8, L / ns);
+    for (int k = 0; k < ns; ++k) {
+      double ang = -kTwoPi * (double)k / (double)(ns * R);
+      h[ns + k] = make_double2(cos(ang), sin(ang));
+    }
+  }
+  if (cudaMalloc(out, sizeof(double2) * h.size()) != cudaSuccess) return VR_ERR_ALLOC;
+  if (cudaMemcpy(*out, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return VR_ERR_ALLOC;
+  return VR_OK;
+}
+
 const size_t kSmemBudget = 200 * 1024;
+
+// ---- fast-path launch helpers (compile-time sizes) ---------------------------------
+#define VR_POW2_SWITCH(L, CASE)                                                                  \
+  switch (L) {                                                                                   \
+    case 8: CASE(8); break;                                                                      \
+    case 16: CASE(16); break;                                                                    \
+    case 32: CASE(32); break;                                                                    \
+    case 64: CASE(64); break;                                                                    \
+    case 128: CASE(128); break;                                                                  \
+    case 256: CASE(256); break;                                                                  \
+    case 512: CASE(512); break;                                                                  \
+    case 1024: CASE(1024); break;                                                                \
+    case 2048: CASE(2048); break;                                                                \
+    default: break;                                                                              \
+  }
+
+template <int L> constexpr size_t fast_lines() { return 2048 / L; }
+constexpr size_t padl(size_t L) { return L + L / 8 + 1; }
+
+size_t sm_z(int M, size_t elem) { return sizeof(double2) * (3 * (size_t)M + 1) + elem * (2048 / M) * padl(M); }
+size_t sm_zi(int M) { return sizeof(double2) * 2 * M + sizeof(float2) * (2048 / M) * padl(M); }
+size_t sm_axis(int L, size_t elem) { return sizeof(double2) * 2 * L + elem * (2048 / L) * padl(L); }
+int xb(int L, int nc) { return (nc == 3 ? 1024 : 2048) / L; }
+size_t sm_x(int L, int nc, size_t elem) { return sizeof(double2) * 2 * L + elem * nc * xb(L, nc) * padl(L); }
+
+template <typename F> void set_smem(F* f, size_t bytes) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void fast_attributes(int n1, int n2, int M) {
+#define A_Z(MM)                                               \
+  set_smem(fast::zfwd_fast<MM, double2>, sm_z(MM, 16));       \
+  set_smem(fast::zfwd_fast<MM, float2>, sm_z(MM, 8));         \
+  set_smem(fast::zinv_fast<MM>, sm_zi(MM));
+#define A_AX(LL)                                              \
+  set_smem(fast::axis_fast<double2, LL, false>, sm_axis(LL, 16)); \
+  set_smem(fast::axis_fast<double2, LL, true>, sm_axis(LL, 16));  \
+  set_smem(fast::axis_fast<float2, LL, false>, sm_axis(LL, 8));   \
+  set_smem(fast::axis_fast<float2, LL, true>, sm_axis(LL, 8));
+#define A_X(LL)                                                        \
+  A_AX(LL)                                                             \
+  set_smem(fast::xop_fast<LL, 3, false, double2>, sm_x(LL, 3, 16));    \
+  set_smem(fast::xop_fast<LL, 3, false, float2>, sm_x(LL, 3, 8));      \
+  set_smem(fast::xop_fast<LL, 1, false, double2>, sm_x(LL, 1, 16));    \
+  set_smem(fast::xop_fast<LL, 1, false, float2>, sm_x(LL, 1, 8));      \
+  set_smem(fast::xop_fast<LL, 1, true, double2>, sm_x(LL, 1, 16));
+  VR_POW2_SWITCH(M, A_Z)
+  VR_POW2_SWITCH(n2, A_AX)
+  VR_POW2_SWITCH(n1, A_X)
+#undef A_Z
+#undef A_AX
+#undef A_X
+}
+
+// Operators whose symbol amplifies high wavenumbers (|k|^2, |k|^4, the H1
+// weights) need the forward transform in f64; bounded symbols
+// (shifted inverses, K, Gaussian) run the forward half in f32.
+bool needs_f64(int kind) { return kind == VR_SPEC_A || kind == VR_SPEC_A2; }
 
 }  // namespace
 
@@ -544,6 +628,7 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   p->d = d;
   p->n3h = d.n3 / 2 + 1;
   p->nspec = (int64_t)d.n1 * d.n2 * p->n3h;
+  p->fast = is_pow2_in(d.n1, 8, 2048) && is_pow2_in(d.n2, 8, 2048) && is_pow2_in(d.n3 / 2, 8, 2048);
   p->rp1 = make_radix_plan(d.n1);
   p->rp2 = make_radix_plan(d.n2);
   p->rp3 = make_radix_plan(d.n3);
@@ -551,6 +636,10 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   rc = upload_twiddles(d.n1, &p->tw1);
   if (!rc) rc = upload_twiddles(d.n2, &p->tw2);
   if (!rc) rc = upload_twiddles(d.n3, &p->tw3);
+  if (!rc) rc = upload_twiddles(d.n3 / 2, &p->tw3h);
+  if (!rc && p->fast) rc = upload_stage_twiddles(d.n1, &p->stw1);
+  if (!rc && p->fast) rc = upload_stage_twiddles(d.n2, &p->stw2);
+  if (!rc && p->fast) rc = upload_stage_twiddles(d.n3 / 2, &p->stw3h);
   if (!rc && cudaMalloc(&p->S, sizeof(double2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
   if (!rc && cudaMalloc(&p->T, sizeof(float2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
   const int maxblk = d.n2 * p->n3h + 1024;
@@ -559,22 +648,20 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
     vr_spec_plan_destroy(p);
     return rc;
   }
-  // tile shapes: ~2-4K complex elements per CTA, within the smem budget
+  // generic path tile shapes: ~2-4K complex elements per CTA within the smem budget
   const size_t kLines = 4096;
   p->RBz = (int)std::max<size_t>(1, std::min<size_t>(16, kLines / d.n3));
   p->RBzi = p->RBz;
   p->smz = sizeof(double2) * (d.n3 + 2 * (size_t)p->RBz * (d.n3 + 1));
   p->smzi = sizeof(double2) * d.n3 + sizeof(float2) * 2 * (size_t)p->RBzi * (d.n3 + 1);
-  p->By = std::min(choose_lines(d.n2, 1, sizeof(double2), 110 * 1024, 16), pow2_floor(p->n3h));
-  p->Byi = std::min(choose_lines(d.n2, 1, sizeof(float2), 110 * 1024, 16), pow2_floor(p->n3h));
-  p->smy = sizeof(double2) * (d.n2 + 2 * (size_t)p->By * (d.n2 + 1));
-  p->smyi = sizeof(double2) * d.n2 + sizeof(float2) * 2 * (size_t)p->Byi * (d.n2 + 1);
   p->Bx3 = std::min(choose_lines(d.n1, 3, sizeof(double2), 110 * 1024, 8), pow2_floor(p->n3h));
   p->Bx1 = std::min(choose_lines(d.n1, 1, sizeof(double2), 110 * 1024, 16), pow2_floor(p->n3h));
   p->smx3 = sizeof(double2) * (d.n1 + 2 * 3 * (size_t)p->Bx3 * (d.n1 + 1));
   p->smx1 = sizeof(double2) * (d.n1 + 2 * 1 * (size_t)p->Bx1 * (d.n1 + 1));
-  if (p->smz > kSmemBudget || p->smzi > kSmemBudget || p->smy > kSmemBudget || p->smyi > kSmemBudget ||
-      p->smx3 > kSmemBudget || p->smx1 > kSmemBudget) {
+  const size_t sy = sizeof(double2) * (d.n2 + 2 * (size_t)choose_lines(d.n2, 1, sizeof(double2), 110 * 1024, 16) *
+                                                 (d.n2 + 1));
+  if (!p->fast && (p->smz > kSmemBudget || p->smzi > kSmemBudget || sy > kSmemBudget ||
+                   p->smx3 > kSmemBudget || p->smx1 > kSmemBudget)) {
     vr_spec_plan_destroy(p);
     return VR_ERR_UNSUPPORTED;
   }
@@ -584,6 +671,7 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   cudaFuncSetAttribute(axis_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
   cudaFuncSetAttribute(x_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
   cudaFuncSetAttribute(x_op_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  if (p->fast) fast_attributes(d.n1, d.n2, d.n3 / 2);
   *out = p;
   return VR_OK;
 }
@@ -593,6 +681,10 @@ int vr_spec_plan_destroy(vr_spec_plan* p) {
   cudaFree(p->tw1);
   cudaFree(p->tw2);
   cudaFree(p->tw3);
+  cudaFree(p->tw3h);
+  cudaFree(p->stw1);
+  cudaFree(p->stw2);
+  cudaFree(p->stw3h);
   cudaFree(p->S);
   cudaFree(p->T);
   cudaFree(p->partials);
@@ -611,6 +703,23 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
   const int64_t es = ax2 ? (int64_t)p->n3h : (int64_t)d.n2 * p->n3h;
   const int n_outer = ax2 ? d.n1 : d.n2;
   const int64_t outer_stride = ax2 ? (int64_t)d.n2 * p->n3h : (int64_t)p->n3h;
+  if (p->fast) {
+    const double2* tw = ax2 ? p->stw2 : p->stw1;
+#define L_AX(LL)                                                                                      \
+  {                                                                                                   \
+    const int B = (int)fast_lines<LL>();                                                              \
+    const int nchunks = (p->n3h + B - 1) / B;                                                         \
+    if (inv)                                                                                          \
+      fast::axis_fast<C, LL, true><<<dim3(n_outer * nchunks, ncomp), 256, sm_axis(LL, sizeof(C)), s>>>( \
+          buf, es, n_outer, outer_stride, p->nspec, p->n3h, tw);                                      \
+    else                                                                                              \
+      fast::axis_fast<C, LL, false><<<dim3(n_outer * nchunks, ncomp), 256, sm_axis(LL, sizeof(C)), s>>>( \
+          buf, es, n_outer, outer_stride, p->nspec, p->n3h, tw);                                      \
+  }
+    VR_POW2_SWITCH(L, L_AX)
+#undef L_AX
+    return;
+  }
   const int B = std::min(choose_lines(L, 1, sizeof(C), 110 * 1024, 16), pow2_floor(p->n3h));
   const size_t sm = sizeof(double2) * L + sizeof(C) * 2 * (size_t)B * (L + 1);
   const int nchunks = (p->n3h + B - 1) / B;
@@ -619,11 +728,34 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
                                                                  ax2 ? p->tw2 : p->tw1, B, inv);
 }
 
-static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s) {
+// forward Z + Y passes into p->S (as double2, or as float2 when !f64 on the fast path)
+static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s, bool f64 = true) {
   const Dims& d = p->d;
   const int nrows = d.n1 * d.n2;
-  fwd_z_kernel<<<dim3((nrows + p->RBz - 1) / p->RBz, ncomp), 256, p->smz, s>>>(in, d, p->n3h, p->rp3, p->tw3,
-                                                                               p->RBz, p->S);
+  if (p->fast) {
+    const int M = d.n3 / 2;
+#define L_Z(MM)                                                                                            \
+  {                                                                                                        \
+    const dim3 g((nrows + (int)fast_lines<MM>() - 1) / (int)fast_lines<MM>(), ncomp);                     \
+    if (f64)                                                                                               \
+      fast::zfwd_fast<MM, double2><<<g, 256, sm_z(MM, 16), s>>>(in, nrows, d.n(), p->nspec, p->stw3h, p->tw3, \
+                                                                p->S);                                     \
+    else                                                                                                   \
+      fast::zfwd_fast<MM, float2><<<g, 256, sm_z(MM, 8), s>>>(in, nrows, d.n(), p->nspec, p->stw3h, p->tw3,  \
+                                                              reinterpret_cast<float2*>(p->S));            \
+  }
+    VR_POW2_SWITCH(M, L_Z)
+#undef L_Z
+    if (f64)
+      launch_axis<double2>(p, p->S, 2, ncomp, 0, s);
+    else
+      launch_axis<float2>(p, reinterpret_cast<float2*>(p->S), 2, ncomp, 0, s);
+    VR_CHECK_LAUNCH();
+    return VR_OK;
+  } else {
+    fwd_z_kernel<<<dim3((nrows + p->RBz - 1) / p->RBz, ncomp), 256, p->smz, s>>>(in, d, p->n3h, p->rp3, p->tw3,
+                                                                                 p->RBz, p->S);
+  }
   launch_axis<double2>(p, p->S, 2, ncomp, 0, s);
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -633,8 +765,60 @@ static void spec_inverse_yz(vr_spec_plan* p, int ncomp, const float* add, float*
   const Dims& d = p->d;
   launch_axis<float2>(p, p->T, 2, ncomp, 1, s);
   const int nrows = d.n1 * d.n2;
+  if (p->fast) {
+    const int M = d.n3 / 2;
+#define L_ZI(MM)                                                                                          \
+  fast::zinv_fast<MM><<<dim3((nrows + (int)fast_lines<MM>() - 1) / (int)fast_lines<MM>(), ncomp), 256,    \
+                        sm_zi(MM), s>>>(p->T, nrows, d.n(), p->nspec, p->stw3h, p->tw3, out, add);
+    VR_POW2_SWITCH(M, L_ZI)
+#undef L_ZI
+    return;
+  }
   inv_z_kernel<<<dim3((nrows + p->RBzi - 1) / p->RBzi, ncomp), 256, p->smzi, s>>>(p->T, d, p->n3h, p->rp3, p->tw3,
                                                                                   p->RBzi, out, add);
+}
+
+// X pass: fwd -> op -> inv (or the H1 reduction); returns number of CTAs
+static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream_t s, bool f64 = true) {
+  const Dims& d = p->d;
+  const int nc = op.ncomp;
+  if (p->fast) {
+    int nblk = 0;
+    float2* S32 = reinterpret_cast<float2*>(p->S);
+#define L_X(LL)                                                                                              \
+  {                                                                                                          \
+    const int B3 = xb(LL, 3), B1 = xb(LL, 1);                                                                \
+    const int B = (nc == 3 && !reduce) ? B3 : B1;                                                            \
+    nblk = d.n2 * ((p->n3h + B - 1) / B);                                                                    \
+    if (reduce)                                                                                              \
+      fast::xop_fast<LL, 1, true, double2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 16), s>>>(                        \
+          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, p->partials);                               \
+    else if (nc == 3 && f64)                                                                                 \
+      fast::xop_fast<LL, 3, false, double2><<<nblk, 3 * B3 * LL / 8, sm_x(LL, 3, 16), s>>>(                  \
+          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                   \
+    else if (nc == 3)                                                                                        \
+      fast::xop_fast<LL, 3, false, float2><<<nblk, 3 * B3 * LL / 8, sm_x(LL, 3, 8), s>>>(                    \
+          S32, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                    \
+    else if (f64)                                                                                            \
+      fast::xop_fast<LL, 1, false, double2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 16), s>>>(                      \
+          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                   \
+    else                                                                                                     \
+      fast::xop_fast<LL, 1, false, float2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 8), s>>>(                        \
+          S32, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                    \
+  }
+    VR_POW2_SWITCH(d.n1, L_X)
+#undef L_X
+    return nblk;
+  }
+  const int B = nc == 3 ? p->Bx3 : p->Bx1;
+  const size_t sm = nc == 3 ? p->smx3 : p->smx1;
+  const int ncx = (p->n3h + B - 1) / B;
+  const int nblk = d.n2 * ncx;
+  if (reduce)
+    x_op_kernel<true><<<nblk, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, p->partials);
+  else
+    x_op_kernel<false><<<nblk, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, nullptr);
+  return nblk;
 }
 
 extern "C" {
@@ -647,13 +831,11 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
-  int rc = spec_forward(p, in, ncomp, s);
+  const bool f64 = needs_f64(kind);
+  int rc = spec_forward(p, in, ncomp, s, f64);
   if (rc) return rc;
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma};
-  const int B = ncomp == 3 ? p->Bx3 : p->Bx1;
-  const size_t sm = ncomp == 3 ? p->smx3 : p->smx1;
-  const int ncx = (p->n3h + B - 1) / B;
-  x_op_kernel<false><<<d.n2 * ncx, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, nullptr);
+  spec_xpass(p, op, false, s, f64);
   spec_inverse_yz(p, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -687,10 +869,7 @@ int vr_h1_energy(vr_spec_plan* p, const float* f, double* out_dev, void* stream)
   int rc = spec_forward(p, f, 1, s);
   if (rc) return rc;
   SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0};
-  const int B = p->Bx1;
-  const int ncx = (p->n3h + B - 1) / B;
-  const int nblk = d.n2 * ncx;
-  x_op_kernel<true><<<nblk, 256, p->smx1, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, p->partials);
+  const int nblk = spec_xpass(p, op, true, s);
   const double n = (double)d.n();
   finalize_sum_kernel<<<1, 1024, 0, s>>>(p->partials, nblk, kTwoPi * kTwoPi * kTwoPi / (n * n), out_dev);
   VR_CHECK_LAUNCH();
