@@ -119,6 +119,114 @@ __device__ __forceinline__ void gather(const Src& src, const Dims& d, int ix, in
     gather_cubic<NC>(src, d, ix, iy, iz, tx, ty, tz, out);
 }
 
+// ---- lean gather for the transport sweeps --------------------------------------
+// Same arithmetic as gather<> but instruction-lean: the base index is wrapped
+// with one conditional per axis (valid while |displacement| < n - 3; callers
+// check and fall back to gather<>), every stencil row gets one 64-bit row
+// pointer and its taps are immediate-offset loads unless the x3 window wraps
+// at the end of the row.
+__device__ __forceinline__ int wrap1(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+template <int ORDER, int NC>
+__device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, const Dims& d, int ix, int iy,
+                                            int iz, float tx, float ty, float tz, float* out) {
+  if (ORDER == ORDER_LINEAR) {
+    const int i0 = wrap1(ix, d.n1), j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
+    const int i1 = next_wrap(i0, d.n1), j1 = next_wrap(j0, d.n2);
+    const bool zin = k0 + 1 < d.n3;
+    const int dk = zin ? 1 : 1 - d.n3;
+    const int r00 = (i0 * d.n2 + j0) * d.n3 + k0, r01 = (i0 * d.n2 + j1) * d.n3 + k0;
+    const int r10 = (i1 * d.n2 + j0) * d.n3 + k0, r11 = (i1 * d.n2 + j1) * d.n3 + k0;
+    const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const float* b = p[c];
+      const float c00 = __ldg(b + r00) * sz + __ldg(b + r00 + dk) * tz;
+      const float c01 = __ldg(b + r01) * sz + __ldg(b + r01 + dk) * tz;
+      const float c10 = __ldg(b + r10) * sz + __ldg(b + r10 + dk) * tz;
+      const float c11 = __ldg(b + r11) * sz + __ldg(b + r11 + dk) * tz;
+      const float c0 = c00 * sy + c01 * ty;
+      const float c1 = c10 * sy + c11 * ty;
+      out[c] = c0 * sx + c1 * tx;
+    }
+  } else {
+    float wx[4], wy[4], wz[4];
+    lagrange4(tx, wx);
+    lagrange4(ty, wy);
+    lagrange4(tz, wz);
+    const int i0 = wrap1(ix, d.n1), j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
+    int xo[4], yo[4];
+    cubic_idx(i0, d.n1, xo);
+    cubic_idx(j0, d.n2, yo);
+    float acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0f;
+    if (k0 >= 1 && k0 + 2 < d.n3) {  // x3 window inside the row: immediate-offset taps
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        float sa[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int row = (xo[a] * d.n2 + yo[b]) * d.n3 + (k0 - 1);   // < 2^31 (dims_from)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const float* r = p[c] + row;
+            const float sb = wz[0] * __ldg(r) + wz[1] * __ldg(r + 1) + wz[2] * __ldg(r + 2) + wz[3] * __ldg(r + 3);
+            sa[c] += wy[b] * sb;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += wx[a] * sa[c];
+      }
+    } else {
+      int zo[4];
+      cubic_idx(k0, d.n3, zo);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        float sa[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int row = (xo[a] * d.n2 + yo[b]) * d.n3;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const float* r = p[c] + row;
+            const float sb = wz[0] * __ldg(r + zo[0]) + wz[1] * __ldg(r + zo[1]) + wz[2] * __ldg(r + zo[2]) +
+                             wz[3] * __ldg(r + zo[3]);
+            sa[c] += wy[b] * sb;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += wx[a] * sa[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c] = acc[c];
+  }
+}
+
+// displacement form for float sources; falls back to the general gather when a
+// displacement is too large for the single-conditional wrap
+template <int ORDER, int NC>
+__device__ __forceinline__ void gather_disp_lean(const float* const* p, const Dims& d, int i, int j, int k, float d1,
+                                                 float d2, float d3, float* out) {
+  int ix, iy, iz;
+  float tx, ty, tz;
+  split_coord(i, d1, ix, tx);
+  split_coord(j, d2, iy, ty);
+  split_coord(k, d3, iz, tz);
+  const bool ok = fabsf(d1) < d.n1 - 4 && fabsf(d2) < d.n2 - 4 && fabsf(d3) < d.n3 - 4;
+  if (ok) {
+    gather_lean<ORDER, NC>(p, d, ix, iy, iz, tx, ty, tz, out);
+  } else {
+    SrcF32 s{{p[0], NC > 1 ? p[1] : p[0], NC > 2 ? p[2] : p[0]}, 0};
+    gather<ORDER, NC>(s, d, ix, iy, iz, tx, ty, tz, out);
+  }
+}
+
 // Gather at voxel (i,j,k) displaced by -(d1,d2,d3) index units.
 template <int ORDER, int NC, class Src>
 __device__ __forceinline__ void gather_disp(const Src& src, const Dims& d, int i, int j, int k, float d1,

@@ -20,6 +20,23 @@ __device__ __forceinline__ void voxel_ijk(int idx, const Dims& d, int& i, int& j
   i = r / d.n2;
 }
 
+// 3-D launch: x = x3 (TPB threads), y = x2, z = x1 -- no index divisions
+struct Vox {
+  int i, j, k, idx;
+  bool ok;
+};
+__device__ __forceinline__ Vox vox3(const Dims& d) {
+  Vox v;
+  v.k = blockIdx.x * blockDim.x + threadIdx.x;
+  v.j = blockIdx.y;
+  v.i = blockIdx.z;
+  v.ok = v.k < d.n3;
+  v.idx = (v.i * d.n2 + v.j) * d.n3 + v.k;
+  return v;
+}
+inline int vox_tpb(const Dims& d) { return d.n3 >= 128 ? 128 : ((d.n3 + 31) / 32) * 32; }
+inline dim3 vox_grid(const Dims& d) { return dim3((d.n3 + vox_tpb(d) - 1) / vox_tpb(d), d.n2, d.n1); }
+
 __device__ __forceinline__ void flag_nonfinite(int* flag, float v) {
   if (flag && !isfinite(v)) atomicOr(flag, 1);
 }
@@ -48,40 +65,39 @@ __global__ void __launch_bounds__(256) interp_points_kernel(const float* __restr
 //   backward trace is the same with -v (transport.py:102)
 //   jac = (1 + dt/2 div(X_f)) / (1 - dt/2 div(x)),  adj likewise with X_b
 template <int ORDER, bool FACTORS>
-__global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
+__global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
                                                     float ih2, float ih3, float* __restrict__ disp_f,
                                                     float* __restrict__ disp_b,
                                                     const float* __restrict__ div,
                                                     float* __restrict__ fac_f, float* __restrict__ fac_b) {
   const int64_t N = d.n();
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= N) return;
-  int i, j, k;
-  voxel_ijk(idx, d, i, j, k);
+  const Vox p = vox3(d);
+  if (!p.ok) return;
+  const int i = p.i, j = p.j, k = p.k, idx = p.idx;
   const float v1 = __ldg(v + idx), v2 = __ldg(v + N + idx), v3 = __ldg(v + 2 * N + idx);
   const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
-  SrcF32 sv{{v, v + N, v + 2 * N}, N};
+  const float* sv[3] = {v, v + N, v + 2 * N};
   float vs[3];
   const float half = 0.5f * dt;
   // forward: x* = x - dt v
-  gather_disp<ORDER, 3>(sv, d, i, j, k, a1, a2, a3, vs);
+  gather_disp_lean<ORDER, 3>(sv, d, i, j, k, a1, a2, a3, vs);
   const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
   disp_f[idx] = f1;
   disp_f[N + idx] = f2;
   disp_f[2 * N + idx] = f3;
   // backward: x* = x + dt v, X = x + dt/2 (v + v(x*))
-  gather_disp<ORDER, 3>(sv, d, i, j, k, -a1, -a2, -a3, vs);
+  gather_disp_lean<ORDER, 3>(sv, d, i, j, k, -a1, -a2, -a3, vs);
   const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
   disp_b[idx] = b1;
   disp_b[N + idx] = b2;
   disp_b[2 * N + idx] = b3;
   if (FACTORS) {
-    SrcF32 sd{{div, div, div}, 0};
+    const float* sd[1] = {div};
     const float denom = 1.0f - half * __ldg(div + idx);
     float dv;
-    gather_disp<ORDER, 1>(sd, d, i, j, k, f1, f2, f3, &dv);
+    gather_disp_lean<ORDER, 1>(sd, d, i, j, k, f1, f2, f3, &dv);
     fac_f[idx] = (1.0f + half * dv) / denom;
-    gather_disp<ORDER, 1>(sd, d, i, j, k, b1, b2, b3, &dv);
+    gather_disp_lean<ORDER, 1>(sd, d, i, j, k, b1, b2, b3, &dv);
     fac_b[idx] = (1.0f + half * dv) / denom;
   }
 }
@@ -91,18 +107,18 @@ __global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v,
 // adjoint: transport.py:154-155 (factor = adj_numer/adj_denom, backward trace)
 // jacobian: transport.py:194-195 (factor = jac_numer/jac_denom)
 template <int ORDER, bool SCALE>
-__global__ void __launch_bounds__(256) advect_kernel(const float* __restrict__ src, Dims d,
+__global__ void __launch_bounds__(128) advect_kernel(const float* __restrict__ src, Dims d,
                                                      const float* __restrict__ disp,
                                                      const float* __restrict__ fac, float* __restrict__ dst,
                                                      int* flag) {
   const int64_t N = d.n();
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= N) return;
-  int i, j, k;
-  voxel_ijk(idx, d, i, j, k);
-  SrcF32 s{{src, src, src}, 0};
+  const Vox p = vox3(d);
+  if (!p.ok) return;
+  const int idx = p.idx;
+  const float* sp[1] = {src};
   float o;
-  gather_disp<ORDER, 1>(s, d, i, j, k, __ldg(disp + idx), __ldg(disp + N + idx), __ldg(disp + 2 * N + idx), &o);
+  gather_disp_lean<ORDER, 1>(sp, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+                             __ldg(disp + 2 * N + idx), &o);
   if (SCALE) o *= __ldg(fac + idx);
   dst[idx] = o;
   flag_nonfinite(flag, o);
@@ -126,19 +142,19 @@ __global__ void __launch_bounds__(256) incstate_init_kernel(const float* __restr
 }
 
 template <int ORDER>
-__global__ void __launch_bounds__(256) incstate_step_kernel(const float* __restrict__ u, Dims d,
+__global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restrict__ u, Dims d,
                                                             const float* __restrict__ disp,
                                                             const float* __restrict__ vt,
                                                             const float* __restrict__ gnext, float half,
                                                             int last, float* __restrict__ out, int* flag) {
   const int64_t N = d.n();
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= N) return;
-  int i, j, k;
-  voxel_ijk(idx, d, i, j, k);
-  SrcF32 s{{u, u, u}, 0};
+  const Vox p = vox3(d);
+  if (!p.ok) return;
+  const int idx = p.idx;
+  const float* sp[1] = {u};
   float o;
-  gather_disp<ORDER, 1>(s, d, i, j, k, __ldg(disp + idx), __ldg(disp + N + idx), __ldg(disp + 2 * N + idx), &o);
+  gather_disp_lean<ORDER, 1>(sp, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+                             __ldg(disp + 2 * N + idx), &o);
   const float hs = half * inc_source(vt, gnext, N, idx);
   float m = o + hs;
   if (last == 0) m = m + hs;
@@ -173,23 +189,22 @@ __global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict
 // step thresholds at 0.5 and writes `id` (labels processed in ascending order, so
 // overlaps resolve to the larger id as in the reference).
 template <int ORDER, bool FROM_LABELS, bool TO_LABELS>
-__global__ void __launch_bounds__(256) label_step_kernel(const float* __restrict__ src,
+__global__ void __launch_bounds__(128) label_step_kernel(const float* __restrict__ src,
                                                          const int* __restrict__ lab_in, int id, Dims d,
                                                          const float* __restrict__ disp,
                                                          float* __restrict__ dst, int* __restrict__ lab_out) {
   const int64_t N = d.n();
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= N) return;
-  int i, j, k;
-  voxel_ijk(idx, d, i, j, k);
+  const Vox p = vox3(d);
+  if (!p.ok) return;
+  const int i = p.i, j = p.j, k = p.k, idx = p.idx;
   float o;
   const float d1 = __ldg(disp + idx), d2 = __ldg(disp + N + idx), d3 = __ldg(disp + 2 * N + idx);
   if (FROM_LABELS) {
     SrcLabel s{lab_in, id};
     gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
   } else {
-    SrcF32 s{{src, src, src}, 0};
-    gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
+    const float* sp[1] = {src};
+    gather_disp_lean<ORDER, 1>(sp, d, i, j, k, d1, d2, d3, &o);
   }
   if (TO_LABELS) {
     if (o >= 0.5f) lab_out[idx] = id;
@@ -264,13 +279,14 @@ int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, fl
   if (factors && (!fac_jac || !fac_adj)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const float ih1 = (float)(d.n1 / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
-  unsigned g = grid_for(d.n(), 256);
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
     if (factors)
-      trace_kernel<ORD, true><<<g, 256, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div, fac_jac,
+      trace_kernel<ORD, true><<<g, tpb, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div, fac_jac,
                                                 fac_adj);
     else
-      trace_kernel<ORD, false><<<g, 256, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, nullptr,
+      trace_kernel<ORD, false><<<g, tpb, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, nullptr,
                                                  nullptr, nullptr);
   });
   VR_CHECK_LAUNCH();
@@ -284,12 +300,13 @@ int vr_advect(const float* src, const int64_t dims[3], const float* disp, const 
   if (rc) return rc;
   if (!src || !disp || !dst || src == dst) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned g = grid_for(d.n(), 256);
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
     if (factor)
-      advect_kernel<ORD, true><<<g, 256, 0, s>>>(src, d, disp, factor, dst, nonfinite_flag);
+      advect_kernel<ORD, true><<<g, tpb, 0, s>>>(src, d, disp, factor, dst, nonfinite_flag);
     else
-      advect_kernel<ORD, false><<<g, 256, 0, s>>>(src, d, disp, nullptr, dst, nonfinite_flag);
+      advect_kernel<ORD, false><<<g, tpb, 0, s>>>(src, d, disp, nullptr, dst, nonfinite_flag);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -315,9 +332,10 @@ int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fw
   if (rc) return rc;
   if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned g = grid_for(d.n(), 256);
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
-    incstate_step_kernel<ORD><<<g, 256, 0, s>>>(u, d, disp_fwd, vt, gradm_next, (float)(0.5 * dt), last, out,
+    incstate_step_kernel<ORD><<<g, tpb, 0, s>>>(u, d, disp_fwd, vt, gradm_next, (float)(0.5 * dt), last, out,
                                                 nonfinite_flag);
   });
   VR_CHECK_LAUNCH();
@@ -343,18 +361,19 @@ int vr_label_step(const float* src, const int* labels_in, int label_id, const in
   if (rc) return rc;
   if (!disp || (!src && !labels_in) || (!dst && !labels_out)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned g = grid_for(d.n(), 256);
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
   const bool from_l = labels_in != nullptr, to_l = labels_out != nullptr;
   VR_DISPATCH_ORDER(order, {
     if (from_l && to_l)
-      label_step_kernel<ORD, true, true><<<g, 256, 0, s>>>(nullptr, labels_in, label_id, d, disp, nullptr,
+      label_step_kernel<ORD, true, true><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, disp, nullptr,
                                                            labels_out);
     else if (from_l)
-      label_step_kernel<ORD, true, false><<<g, 256, 0, s>>>(nullptr, labels_in, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, true, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, disp, dst, nullptr);
     else if (to_l)
-      label_step_kernel<ORD, false, true><<<g, 256, 0, s>>>(src, nullptr, label_id, d, disp, nullptr, labels_out);
+      label_step_kernel<ORD, false, true><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, disp, nullptr, labels_out);
     else
-      label_step_kernel<ORD, false, false><<<g, 256, 0, s>>>(src, nullptr, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, false, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, disp, dst, nullptr);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
