@@ -99,3 +99,18 @@ def test_pcg_exact_preconditioner(P):
     assert info.converged and info.iterations == 1
     r = mv(x).data - rhs.data
     assert float(torch.linalg.norm(r) / torch.linalg.norm(rhs.data)) < 1e-5
+
+
+def test_register_c2_256(P):
+    """C2 at full size (256^3) against the live reference's 591 s CPU run
+    (tests/golden/c2_256.json): same PCG counts, residual / objectives within
+    1e-3, Dice within 0.5 pp."""
+    from paper_2209_08189_b200.synth import c2_problem
+    gold = golden_json("c2_256.json")
+    g = P.make_grid((256, 256, 256))
+    m0, m1, l0, l1, _ = c2_problem(g)
+    res = P.register(m0, m1, P.RegistrationConfig(beta_v=1e-2, beta_w=0.0, n_t=4, interp_order="cubic"),
+                     labels0=l0, labels1=l1, pre_dice=True)
+    _check(res.diagnostics, gold["run"])
+    assert abs(res.dice_pre.d_a - gold["dice_pre"]) < 0.005
+    assert abs(res.dice.d_a - gold["dice_post"]) < 0.005
