@@ -139,6 +139,41 @@ int vr_fill(int64_t n, float value, float* out, void* stream);
 int vr_label_counts(const int* l0, const int* l1, int64_t n, int max_id, unsigned long long* counts,
                     void* stream);
 
+/* ---- x1-slab (multi-GPU) variants ---------------------------------------------
+ * A rank owns x1 planes [r*L1, (r+1)*L1) of every field.  `*_ext` inputs carry
+ * `xoff` ghost planes on each side (filled by the host's NCCL halo exchange,
+ * paper_2209_08189_b200/dist.py); dims are the LOCAL (L1, N2, N3); outputs are
+ * local.  The ghost width must cover the largest x1 displacement plus the
+ * stencil (the host sizes it from an allreduce-max). */
+int vr_trace_rk2_slab(const float* v_ext, const int64_t dims4[4] /* L1,N2,N3,N1 */, int xoff, double dt, int order,
+                      float* disp_fwd, float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj,
+                      void* stream);
+int vr_advect_slab(const float* src_ext, const int64_t dims[3], int xoff, const float* disp, const float* factor,
+                   int order, float* dst, int* nonfinite_flag, void* stream);
+int vr_incstate_step_slab(const float* u_ext, const int64_t dims[3], int xoff, const float* disp_fwd,
+                          const float* vt, const float* gradm_next, double dt, int order, int last, float* out,
+                          int* nonfinite_flag, void* stream);
+int vr_label_step_slab(const float* src_ext, int label_id, const int64_t dims[3], int xoff, const float* disp,
+                       int order, float* dst, int* labels_out, void* stream);
+int vr_fd8_grad_slab(const float* f_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out3,
+                     void* stream);
+int vr_fd8_div_slab(const float* v3_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out,
+                    void* stream);
+
+/* distributed spectral operator = forward (x3, x2 local + pack) -> host
+ * all-to-all per component -> X pass on x1 lines -> host all-to-all back ->
+ * inverse (unpack + x2, x3).  pl: plan of the local slab (L1, N2, N3); px: plan
+ * of the transposed block (N1, N2/P, N3).  Power-of-two sizes only. */
+int vr_spec_plan_is_fast(const vr_spec_plan* plan);
+int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, void* sendbuf, void* stream);
+int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
+                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, const void* recv, void* xout,
+                   void* stream);
+int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, double scale, double* out_dev,
+                        void* stream);
+int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

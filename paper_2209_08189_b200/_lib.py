@@ -54,6 +54,18 @@ _SIGS = {
     "vr_pcg_update": [_i64, _f64, _p, _p, _p, _p, _p],
     "vr_fill": [_i64, _f32, _p, _p],
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
+    # x1-slab / distributed
+    "vr_trace_rk2_slab": [_p, _dims_t, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
+    "vr_advect_slab": [_p, _dims_t, _i32, _p, _p, _i32, _p, _p, _p],
+    "vr_incstate_step_slab": [_p, _dims_t, _i32, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
+    "vr_label_step_slab": [_p, _i32, _dims_t, _i32, _p, _i32, _p, _p, _p],
+    "vr_fd8_grad_slab": [_p, _dims_t, _i32, _i64, _p, _p],
+    "vr_fd8_div_slab": [_p, _dims_t, _i32, _i64, _p, _p],
+    "vr_spec_plan_is_fast": [_p],
+    "vr_dspec_forward": [_p, _p, _i32, _i32, _i32, _p, _p],
+    "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _p, _p, _p],
+    "vr_dspec_h1_partial": [_p, _p, _i32, _i32, _f64, _p, _p],
+    "vr_dspec_inverse": [_p, _p, _i32, _i32, _p, _p, _p],
 }
 
 EXPORTED = tuple(_SIGS)
@@ -71,6 +83,8 @@ class NativeError(VelregError):
 
 # kernels launched per C-ABI call (for the bench's gpu_launches accounting)
 LAUNCHES = {"vr_spec_apply": 5, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2,
+            "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
+            "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
             "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0}
 

@@ -121,22 +121,26 @@ __device__ __forceinline__ void gather(const Src& src, const Dims& d, int ix, in
 
 // ---- lean gather for the transport sweeps --------------------------------------
 // Same arithmetic as gather<> but instruction-lean: the base index is wrapped
-// with one conditional per axis (valid while |displacement| < n - 3; callers
-// check and fall back to gather<>), every stencil row gets one 64-bit row
-// pointer and its taps are immediate-offset loads unless the x3 window wraps
-// at the end of the row.
+// with one conditional per axis, every stencil row gets one row index and its
+// taps are immediate-offset loads unless the x3 window wraps at the end of the
+// row.  SLAB: the source is an x1 slab with `xoff` ghost planes on each side
+// (multi-GPU decomposition, dist.py): x1 is offset, never wrapped, and clamped
+// into the slab (the ghost width is sized from the global max displacement).
 __device__ __forceinline__ int wrap1(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+__device__ __forceinline__ int clampi(int i, int lo, int hi) { return i < lo ? lo : (i > hi ? hi : i); }
 
-template <int ORDER, int NC>
-__device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, const Dims& d, int ix, int iy,
+template <int ORDER, int NC, bool SLAB>
+__device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, const Dims& ds, int ix, int iy,
                                             int iz, float tx, float ty, float tz, float* out) {
+  // ds = SOURCE dims (for SLAB, ds.n1 includes the ghost planes and ix is already offset)
   if (ORDER == ORDER_LINEAR) {
-    const int i0 = wrap1(ix, d.n1), j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
-    const int i1 = next_wrap(i0, d.n1), j1 = next_wrap(j0, d.n2);
-    const bool zin = k0 + 1 < d.n3;
-    const int dk = zin ? 1 : 1 - d.n3;
-    const int r00 = (i0 * d.n2 + j0) * d.n3 + k0, r01 = (i0 * d.n2 + j1) * d.n3 + k0;
-    const int r10 = (i1 * d.n2 + j0) * d.n3 + k0, r11 = (i1 * d.n2 + j1) * d.n3 + k0;
+    const int i0 = SLAB ? clampi(ix, 0, ds.n1 - 2) : wrap1(ix, ds.n1);
+    const int j0 = wrap1(iy, ds.n2), k0 = wrap1(iz, ds.n3);
+    const int i1 = SLAB ? i0 + 1 : next_wrap(i0, ds.n1), j1 = next_wrap(j0, ds.n2);
+    const bool zin = k0 + 1 < ds.n3;
+    const int dk = zin ? 1 : 1 - ds.n3;
+    const int r00 = (i0 * ds.n2 + j0) * ds.n3 + k0, r01 = (i0 * ds.n2 + j1) * ds.n3 + k0;
+    const int r10 = (i1 * ds.n2 + j0) * ds.n3 + k0, r11 = (i1 * ds.n2 + j1) * ds.n3 + k0;
     const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -154,14 +158,19 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
     lagrange4(tx, wx);
     lagrange4(ty, wy);
     lagrange4(tz, wz);
-    const int i0 = wrap1(ix, d.n1), j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
+    const int j0 = wrap1(iy, ds.n2), k0 = wrap1(iz, ds.n3);
     int xo[4], yo[4];
-    cubic_idx(i0, d.n1, xo);
-    cubic_idx(j0, d.n2, yo);
+    if (SLAB) {
+      const int i0 = clampi(ix, 1, ds.n1 - 3);
+      xo[0] = i0 - 1; xo[1] = i0; xo[2] = i0 + 1; xo[3] = i0 + 2;
+    } else {
+      cubic_idx(wrap1(ix, ds.n1), ds.n1, xo);
+    }
+    cubic_idx(j0, ds.n2, yo);
     float acc[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = 0.0f;
-    if (k0 >= 1 && k0 + 2 < d.n3) {  // x3 window inside the row: immediate-offset taps
+    if (k0 >= 1 && k0 + 2 < ds.n3) {  // x3 window inside the row: immediate-offset taps
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         float sa[NC];
@@ -169,7 +178,7 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
         for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int row = (xo[a] * d.n2 + yo[b]) * d.n3 + (k0 - 1);   // < 2^31 (dims_from)
+          const int row = (xo[a] * ds.n2 + yo[b]) * ds.n3 + (k0 - 1);   // < 2^31 (dims_from)
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             const float* r = p[c] + row;
@@ -182,7 +191,7 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
       }
     } else {
       int zo[4];
-      cubic_idx(k0, d.n3, zo);
+      cubic_idx(k0, ds.n3, zo);
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         float sa[NC];
@@ -190,7 +199,7 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
         for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int row = (xo[a] * d.n2 + yo[b]) * d.n3;
+          const int row = (xo[a] * ds.n2 + yo[b]) * ds.n3;
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             const float* r = p[c] + row;
@@ -208,23 +217,27 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
   }
 }
 
-// displacement form for float sources; falls back to the general gather when a
-// displacement is too large for the single-conditional wrap
-template <int ORDER, int NC>
-__device__ __forceinline__ void gather_disp_lean(const float* const* p, const Dims& d, int i, int j, int k, float d1,
-                                                 float d2, float d3, float* out) {
+// Departure point of arrival voxel (i,j,k) (local index) displaced by -(d1,d2,d3).
+// d = ARRIVAL dims; the source has d.n1 + 2*xoff x1 planes when SLAB.  Huge
+// displacements (|d| >= n - 4) are pre-wrapped with a full modulo.
+template <int ORDER, int NC, bool SLAB>
+__device__ __forceinline__ void gather_disp_lean(const float* const* p, const Dims& d, int xoff, int i, int j, int k,
+                                                 float d1, float d2, float d3, float* out) {
   int ix, iy, iz;
   float tx, ty, tz;
   split_coord(i, d1, ix, tx);
   split_coord(j, d2, iy, ty);
   split_coord(k, d3, iz, tz);
-  const bool ok = fabsf(d1) < d.n1 - 4 && fabsf(d2) < d.n2 - 4 && fabsf(d3) < d.n3 - 4;
-  if (ok) {
-    gather_lean<ORDER, NC>(p, d, ix, iy, iz, tx, ty, tz, out);
-  } else {
-    SrcF32 s{{p[0], NC > 1 ? p[1] : p[0], NC > 2 ? p[2] : p[0]}, 0};
-    gather<ORDER, NC>(s, d, ix, iy, iz, tx, ty, tz, out);
+  Dims ds = d;
+  if (SLAB) {
+    ds.n1 = d.n1 + 2 * xoff;
+    ix += xoff;
+  } else if (!(fabsf(d1) < d.n1 - 4)) {
+    ix = wrap_idx(ix, d.n1);
   }
+  if (!(fabsf(d2) < d.n2 - 4)) iy = wrap_idx(iy, d.n2);
+  if (!(fabsf(d3) < d.n3 - 4)) iz = wrap_idx(iz, d.n3);
+  gather_lean<ORDER, NC, SLAB>(p, ds, ix, iy, iz, tx, ty, tz, out);
 }
 
 // Gather at voxel (i,j,k) displaced by -(d1,d2,d3) index units.

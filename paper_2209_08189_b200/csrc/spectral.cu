@@ -206,6 +206,7 @@ struct SpecOp {
   int kind;
   int ncomp;
   double beta_v, beta_w, shift, scale, sigma;
+  int j0, n2g;   // x2 offset / global x2 size of this tile (distributed transposed X pass)
 };
 
 __device__ __forceinline__ int signed_freq(int m, int n) { return m < n / 2 ? m : m - n; }  // fftfreq*n
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(256) x_op_kernel(const double2* __restrict__ S
   __syncthreads();
   double2* res = line_fft<double2>(a, b, ls, NC * B, rp, tw_s, false);
   double2* other = (res == a) ? b : a;
-  const double k2 = (double)signed_freq(j, d.n2);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g);
   if (REDUCE) {
     double acc = 0.0;
     for (int t = threadIdx.x; t < L * nb; t += blockDim.x) {
@@ -779,12 +780,15 @@ static void spec_inverse_yz(vr_spec_plan* p, int ncomp, const float* add, float*
 }
 
 // X pass: fwd -> op -> inv (or the H1 reduction); returns number of CTAs
-static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream_t s, bool f64 = true) {
+static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream_t s, bool f64 = true,
+                      const void* Sext = nullptr, float2* Text = nullptr) {
   const Dims& d = p->d;
   const int nc = op.ncomp;
+  const double2* Sd = Sext ? reinterpret_cast<const double2*>(Sext) : p->S;
+  float2* Tt = Text ? Text : p->T;
   if (p->fast) {
     int nblk = 0;
-    float2* S32 = reinterpret_cast<float2*>(p->S);
+    const float2* S32 = reinterpret_cast<const float2*>(Sd);
 #define L_X(LL)                                                                                              \
   {                                                                                                          \
     const int B3 = xb(LL, 3), B1 = xb(LL, 1);                                                                \
@@ -792,19 +796,19 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
     nblk = d.n2 * ((p->n3h + B - 1) / B);                                                                    \
     if (reduce)                                                                                              \
       fast::xop_fast<LL, 1, true, double2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 16), s>>>(                        \
-          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, p->partials);                               \
+          Sd, Tt, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, p->partials);                                   \
     else if (nc == 3 && f64)                                                                                 \
       fast::xop_fast<LL, 3, false, double2><<<nblk, 3 * B3 * LL / 8, sm_x(LL, 3, 16), s>>>(                  \
-          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                   \
+          Sd, Tt, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                       \
     else if (nc == 3)                                                                                        \
       fast::xop_fast<LL, 3, false, float2><<<nblk, 3 * B3 * LL / 8, sm_x(LL, 3, 8), s>>>(                    \
-          S32, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                    \
+          S32, Tt, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                      \
     else if (f64)                                                                                            \
       fast::xop_fast<LL, 1, false, double2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 16), s>>>(                      \
-          p->S, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                   \
+          Sd, Tt, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                       \
     else                                                                                                     \
       fast::xop_fast<LL, 1, false, float2><<<nblk, B1 * LL / 8, sm_x(LL, 1, 8), s>>>(                        \
-          S32, p->T, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                    \
+          S32, Tt, d.n2, d.n3, p->n3h, p->nspec, p->stw1, op, nullptr);                                      \
   }
     VR_POW2_SWITCH(d.n1, L_X)
 #undef L_X
@@ -815,9 +819,9 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   const int ncx = (p->n3h + B - 1) / B;
   const int nblk = d.n2 * ncx;
   if (reduce)
-    x_op_kernel<true><<<nblk, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, p->partials);
+    x_op_kernel<true><<<nblk, 256, sm, s>>>(Sd, Tt, d, p->n3h, p->rp1, p->tw1, B, op, p->partials);
   else
-    x_op_kernel<false><<<nblk, 256, sm, s>>>(p->S, p->T, d, p->n3h, p->rp1, p->tw1, B, op, nullptr);
+    x_op_kernel<false><<<nblk, 256, sm, s>>>(Sd, Tt, d, p->n3h, p->rp1, p->tw1, B, op, nullptr);
   return nblk;
 }
 
@@ -834,7 +838,7 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   const bool f64 = needs_f64(kind);
   int rc = spec_forward(p, in, ncomp, s, f64);
   if (rc) return rc;
-  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma};
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma, 0, d.n2};
   spec_xpass(p, op, false, s, f64);
   spec_inverse_yz(p, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
@@ -868,7 +872,7 @@ int vr_h1_energy(vr_spec_plan* p, const float* f, double* out_dev, void* stream)
   const Dims& d = p->d;
   int rc = spec_forward(p, f, 1, s);
   if (rc) return rc;
-  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0};
+  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, 0, d.n2};
   const int nblk = spec_xpass(p, op, true, s);
   const double n = (double)d.n();
   finalize_sum_kernel<<<1, 1024, 0, s>>>(p->partials, nblk, kTwoPi * kTwoPi * kTwoPi / (n * n), out_dev);
@@ -883,5 +887,120 @@ int vr_spec_plan_dims(const vr_spec_plan* p, int64_t dims_out[3]) {
   dims_out[2] = p->d.n3;
   return VR_OK;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------
+// Distributed (x1-slab) spectral operators.  A rank owns x1 planes [r L1, (r+1) L1)
+// of the real fields.  Forward: x3 and x2 passes on the local slab, then the
+// half spectrum is packed per destination rank q (x2 block [q L2, (q+1) L2)) so
+// that ONE all-to-all per component (torch.distributed / NCCL, issued by the
+// host) delivers complete x1 lines: recv[c][x1 = p L1 + i][jl][kz].  The X pass
+// (forward, symbol, inverse) runs on that transposed block with the x2
+// wavenumber offset j0 = r L2; its output is already contiguous per destination
+// for the inverse all-to-all; the receiver unpacks and runs the x2 / x3 inverse
+// passes.  Requires the power-of-two fast path on both plans.
+// ---------------------------------------------------------------------------------
+namespace vr {
+
+template <typename C>
+__global__ void pack_kernel(const C* __restrict__ S, C* __restrict__ out, int ncomp, int L1, int N2, int n3h, int P) {
+  const int L2 = N2 / P;
+  const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    // out layout [c][q][i][jl][kz]
+    int64_t r = e;
+    const int kz = (int)(r % n3h); r /= n3h;
+    const int jl = (int)(r % L2); r /= L2;
+    const int i = (int)(r % L1); r /= L1;
+    const int q = (int)(r % P);
+    const int c = (int)(r / P);
+    out[e] = S[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz];
+  }
+}
+
+__global__ void unpack_kernel(const float2* __restrict__ in, float2* __restrict__ T, int ncomp, int L1, int N2, int n3h,
+                              int P) {
+  const int L2 = N2 / P;
+  const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    // in layout [c][q][i][jl][kz]
+    int64_t r = e;
+    const int kz = (int)(r % n3h); r /= n3h;
+    const int jl = (int)(r % L2); r /= L2;
+    const int i = (int)(r % L1); r /= L1;
+    const int q = (int)(r % P);
+    const int c = (int)(r / P);
+    T[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz] = in[e];
+  }
+}
+
+}  // namespace vr
+
+extern "C" {
+
+// Z + Y forward passes of `in` (local slab, ncomp components) and pack into
+// sendbuf ([c][q][i][jl][kz], complex128 if f64 else complex64).
+int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, void* sendbuf, void* stream) {
+  if (!pl || !in || !sendbuf || nranks < 1 || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = spec_forward(pl, in, ncomp, s, f64 != 0);
+  if (rc) return rc;
+  const int64_t n = pl->nspec * ncomp;
+  if (f64)
+    pack_kernel<double2><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(pl->S, reinterpret_cast<double2*>(sendbuf), ncomp,
+                                                                   pl->d.n1, pl->d.n2, pl->n3h, nranks);
+  else
+    pack_kernel<float2><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(reinterpret_cast<const float2*>(pl->S),
+                                                                  reinterpret_cast<float2*>(sendbuf), ncomp, pl->d.n1,
+                                                                  pl->d.n2, pl->n3h, nranks);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// X pass on the transposed block (px dims = {N1, L2, N3}); recv / xout are
+// [c][x1][jl][kz]; n_global = N1*N2*N3 for the inverse normalisation.
+int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
+                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, const void* recv, void* xout,
+                   void* stream) {
+  if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
+  if (!px->fast) return VR_ERR_UNSUPPORTED;
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global};
+  spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, reinterpret_cast<float2*>(xout));
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// H1 partial sum over this rank's transposed block -> *out_dev = scale * sum
+int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, double scale, double* out_dev,
+                        void* stream) {
+  if (!px || !recv || !out_dev) return VR_ERR_ARG;
+  if (!px->fast) return VR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, j0, n2_global};
+  const int nblk = spec_xpass(px, op, true, s, true, recv, nullptr);
+  finalize_sum_kernel<<<1, 1024, 0, s>>>(px->partials, nblk, scale, out_dev);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// unpack the inverse all-to-all result ([c][q][i][jl][kz], complex64) and run the
+// Y / Z inverse passes into `out` (+ add) on the local slab
+int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
+                     void* stream) {
+  if (!pl || !recv_inv || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = pl->nspec * ncomp;
+  unpack_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(reinterpret_cast<const float2*>(recv_inv), pl->T, ncomp,
+                                                           pl->d.n1, pl->d.n2, pl->n3h, nranks);
+  spec_inverse_yz(pl, ncomp, add, out, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_spec_plan_is_fast(const vr_spec_plan* p) { return p && p->fast ? 1 : 0; }
 
 }  // extern "C"

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(NC == 3 ? 384 : 256, NC == 3 ? 2 : 3) xop_fast
   __syncthreads();
   fft_tile<CF, L, false>(tile, tw_s);
   __syncthreads();
-  const double k2 = (double)signed_freq(j, n2);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g);
   if constexpr (REDUCE) {
     double acc = 0.0;
     for (int t = threadIdx.x; t < L * nb; t += NT) {

@@ -64,40 +64,43 @@ __global__ void __launch_bounds__(256) interp_points_kernel(const float* __restr
 //   x* = x - dt v(x);  X = x - dt/2 (v(x) + v(x*))           (forward)
 //   backward trace is the same with -v (transport.py:102)
 //   jac = (1 + dt/2 div(X_f)) / (1 - dt/2 div(x)),  adj likewise with X_b
-template <int ORDER, bool FACTORS>
-__global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
-                                                    float ih2, float ih3, float* __restrict__ disp_f,
-                                                    float* __restrict__ disp_b,
+// SLAB: v / div are x1 slabs with `xoff` ghost planes per side (component
+// stride Ne); outputs are the local slab.
+template <int ORDER, bool FACTORS, bool SLAB>
+__global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v, Dims d, int xoff, int64_t Ne,
+                                                    float dt, float ih1, float ih2, float ih3,
+                                                    float* __restrict__ disp_f, float* __restrict__ disp_b,
                                                     const float* __restrict__ div,
                                                     float* __restrict__ fac_f, float* __restrict__ fac_b) {
   const int64_t N = d.n();
   const Vox p = vox3(d);
   if (!p.ok) return;
   const int i = p.i, j = p.j, k = p.k, idx = p.idx;
-  const float v1 = __ldg(v + idx), v2 = __ldg(v + N + idx), v3 = __ldg(v + 2 * N + idx);
+  const int sidx = SLAB ? idx + xoff * d.n2 * d.n3 : idx;   // own voxel in the source slab
+  const float v1 = __ldg(v + sidx), v2 = __ldg(v + Ne + sidx), v3 = __ldg(v + 2 * Ne + sidx);
   const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
-  const float* sv[3] = {v, v + N, v + 2 * N};
+  const float* sv[3] = {v, v + Ne, v + 2 * Ne};
   float vs[3];
   const float half = 0.5f * dt;
   // forward: x* = x - dt v
-  gather_disp_lean<ORDER, 3>(sv, d, i, j, k, a1, a2, a3, vs);
+  gather_disp_lean<ORDER, 3, SLAB>(sv, d, xoff, i, j, k, a1, a2, a3, vs);
   const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
   disp_f[idx] = f1;
   disp_f[N + idx] = f2;
   disp_f[2 * N + idx] = f3;
   // backward: x* = x + dt v, X = x + dt/2 (v + v(x*))
-  gather_disp_lean<ORDER, 3>(sv, d, i, j, k, -a1, -a2, -a3, vs);
+  gather_disp_lean<ORDER, 3, SLAB>(sv, d, xoff, i, j, k, -a1, -a2, -a3, vs);
   const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
   disp_b[idx] = b1;
   disp_b[N + idx] = b2;
   disp_b[2 * N + idx] = b3;
   if (FACTORS) {
     const float* sd[1] = {div};
-    const float denom = 1.0f - half * __ldg(div + idx);
+    const float denom = 1.0f - half * __ldg(div + sidx);
     float dv;
-    gather_disp_lean<ORDER, 1>(sd, d, i, j, k, f1, f2, f3, &dv);
+    gather_disp_lean<ORDER, 1, SLAB>(sd, d, xoff, i, j, k, f1, f2, f3, &dv);
     fac_f[idx] = (1.0f + half * dv) / denom;
-    gather_disp_lean<ORDER, 1>(sd, d, i, j, k, b1, b2, b3, &dv);
+    gather_disp_lean<ORDER, 1, SLAB>(sd, d, xoff, i, j, k, b1, b2, b3, &dv);
     fac_b[idx] = (1.0f + half * dv) / denom;
   }
 }
@@ -106,8 +109,8 @@ __global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v,
 // state  : transport.py:130-133 (no factor)
 // adjoint: transport.py:154-155 (factor = adj_numer/adj_denom, backward trace)
 // jacobian: transport.py:194-195 (factor = jac_numer/jac_denom)
-template <int ORDER, bool SCALE>
-__global__ void __launch_bounds__(128) advect_kernel(const float* __restrict__ src, Dims d,
+template <int ORDER, bool SCALE, bool SLAB>
+__global__ void __launch_bounds__(128) advect_kernel(const float* __restrict__ src, Dims d, int xoff,
                                                      const float* __restrict__ disp,
                                                      const float* __restrict__ fac, float* __restrict__ dst,
                                                      int* flag) {
@@ -117,8 +120,8 @@ __global__ void __launch_bounds__(128) advect_kernel(const float* __restrict__ s
   const int idx = p.idx;
   const float* sp[1] = {src};
   float o;
-  gather_disp_lean<ORDER, 1>(sp, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
-                             __ldg(disp + 2 * N + idx), &o);
+  gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+                                   __ldg(disp + 2 * N + idx), &o);
   if (SCALE) o *= __ldg(fac + idx);
   dst[idx] = o;
   flag_nonfinite(flag, o);
@@ -141,8 +144,8 @@ __global__ void __launch_bounds__(256) incstate_init_kernel(const float* __restr
   u0[idx] = half * inc_source(vt, g0, N, idx);
 }
 
-template <int ORDER>
-__global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restrict__ u, Dims d,
+template <int ORDER, bool SLAB>
+__global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restrict__ u, Dims d, int xoff,
                                                             const float* __restrict__ disp,
                                                             const float* __restrict__ vt,
                                                             const float* __restrict__ gnext, float half,
@@ -153,8 +156,8 @@ __global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restr
   const int idx = p.idx;
   const float* sp[1] = {u};
   float o;
-  gather_disp_lean<ORDER, 1>(sp, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
-                             __ldg(disp + 2 * N + idx), &o);
+  gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+                                   __ldg(disp + 2 * N + idx), &o);
   const float hs = half * inc_source(vt, gnext, N, idx);
   float m = o + hs;
   if (last == 0) m = m + hs;
@@ -188,9 +191,9 @@ __global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict
 // First step gathers the indicator of `id` straight from the label map; the last
 // step thresholds at 0.5 and writes `id` (labels processed in ascending order, so
 // overlaps resolve to the larger id as in the reference).
-template <int ORDER, bool FROM_LABELS, bool TO_LABELS>
+template <int ORDER, bool FROM_LABELS, bool TO_LABELS, bool SLAB>
 __global__ void __launch_bounds__(128) label_step_kernel(const float* __restrict__ src,
-                                                         const int* __restrict__ lab_in, int id, Dims d,
+                                                         const int* __restrict__ lab_in, int id, Dims d, int xoff,
                                                          const float* __restrict__ disp,
                                                          float* __restrict__ dst, int* __restrict__ lab_out) {
   const int64_t N = d.n();
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(128) label_step_kernel(const float* __restrict
     gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
   } else {
     const float* sp[1] = {src};
-    gather_disp_lean<ORDER, 1>(sp, d, i, j, k, d1, d2, d3, &o);
+    gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, i, j, k, d1, d2, d3, &o);
   }
   if (TO_LABELS) {
     if (o >= 0.5f) lab_out[idx] = id;
@@ -269,8 +272,11 @@ int vr_interp_points(const float* src, const int64_t dims[3], const void* pts, i
   return VR_OK;
 }
 
-int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, float* disp_fwd, float* disp_bwd,
-                 const float* div, float* fac_jac, float* fac_adj, void* stream) {
+}  // extern "C"
+
+// xoff < 0: periodic single-domain call; xoff >= 0: x1 slab with xoff ghost planes
+static int trace_impl(const float* v, const int64_t dims[3], int xoff, double dt, int order, float* disp_fwd,
+                      float* disp_bwd, const float* div, float* fac_jac, float* fac_adj, void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
@@ -278,23 +284,35 @@ int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, fl
   const bool factors = div != nullptr;
   if (factors && (!fac_jac || !fac_adj)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  // spacing of the GLOBAL lattice: for a slab call dims[0] is the local plane
+  // count, the x1 spacing is passed through dims[3] (global N1) by the slab entry
   const float ih1 = (float)(d.n1 / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
+  const int64_t Ne = (int64_t)(d.n1 + 2 * (xoff > 0 ? xoff : 0)) * d.n2 * d.n3;
   VR_DISPATCH_ORDER(order, {
-    if (factors)
-      trace_kernel<ORD, true><<<g, tpb, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div, fac_jac,
-                                                fac_adj);
-    else
-      trace_kernel<ORD, false><<<g, tpb, 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, nullptr,
-                                                 nullptr, nullptr);
+    if (xoff >= 0) {
+      const float gih1 = (float)(dims[3] / kTwoPi);
+      if (factors)
+        trace_kernel<ORD, true, true><<<g, tpb, 0, s>>>(v, d, xoff, Ne, (float)dt, gih1, ih2, ih3, disp_fwd,
+                                                        disp_bwd, div, fac_jac, fac_adj);
+      else
+        trace_kernel<ORD, false, true><<<g, tpb, 0, s>>>(v, d, xoff, Ne, (float)dt, gih1, ih2, ih3, disp_fwd,
+                                                         disp_bwd, nullptr, nullptr, nullptr);
+    } else if (factors) {
+      trace_kernel<ORD, true, false><<<g, tpb, 0, s>>>(v, d, 0, Ne, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                       div, fac_jac, fac_adj);
+    } else {
+      trace_kernel<ORD, false, false><<<g, tpb, 0, s>>>(v, d, 0, Ne, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                        nullptr, nullptr, nullptr);
+    }
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
-int vr_advect(const float* src, const int64_t dims[3], const float* disp, const float* factor, int order,
-              float* dst, int* nonfinite_flag, void* stream) {
+static int advect_impl(const float* src, const int64_t dims[3], int xoff, const float* disp, const float* factor,
+                       int order, float* dst, int* nonfinite_flag, void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
@@ -303,13 +321,67 @@ int vr_advect(const float* src, const int64_t dims[3], const float* disp, const 
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
-    if (factor)
-      advect_kernel<ORD, true><<<g, tpb, 0, s>>>(src, d, disp, factor, dst, nonfinite_flag);
-    else
-      advect_kernel<ORD, false><<<g, tpb, 0, s>>>(src, d, disp, nullptr, dst, nonfinite_flag);
+    if (xoff >= 0) {
+      if (factor)
+        advect_kernel<ORD, true, true><<<g, tpb, 0, s>>>(src, d, xoff, disp, factor, dst, nonfinite_flag);
+      else
+        advect_kernel<ORD, false, true><<<g, tpb, 0, s>>>(src, d, xoff, disp, nullptr, dst, nonfinite_flag);
+    } else if (factor) {
+      advect_kernel<ORD, true, false><<<g, tpb, 0, s>>>(src, d, 0, disp, factor, dst, nonfinite_flag);
+    } else {
+      advect_kernel<ORD, false, false><<<g, tpb, 0, s>>>(src, d, 0, disp, nullptr, dst, nonfinite_flag);
+    }
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
+}
+
+static int incstate_impl(const float* u, const int64_t dims[3], int xoff, const float* disp_fwd, const float* vt,
+                         const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
+                         void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
+  VR_DISPATCH_ORDER(order, {
+    if (xoff >= 0)
+      incstate_step_kernel<ORD, true><<<g, tpb, 0, s>>>(u, d, xoff, disp_fwd, vt, gradm_next, (float)(0.5 * dt),
+                                                        last, out, nonfinite_flag);
+    else
+      incstate_step_kernel<ORD, false><<<g, tpb, 0, s>>>(u, d, 0, disp_fwd, vt, gradm_next, (float)(0.5 * dt),
+                                                         last, out, nonfinite_flag);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+extern "C" {
+
+int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, float* disp_fwd, float* disp_bwd,
+                 const float* div, float* fac_jac, float* fac_adj, void* stream) {
+  return trace_impl(v, dims, -1, dt, order, disp_fwd, disp_bwd, div, fac_jac, fac_adj, stream);
+}
+
+// x1-slab variant: dims4 = {L1 (local planes), N2, N3, N1 (global planes)};
+// v (3 comps) and div carry `xoff` ghost planes on each side.
+int vr_trace_rk2_slab(const float* v_ext, const int64_t dims4[4], int xoff, double dt, int order, float* disp_fwd,
+                      float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj, void* stream) {
+  if (xoff < 0) return VR_ERR_ARG;
+  return trace_impl(v_ext, dims4, xoff, dt, order, disp_fwd, disp_bwd, div_ext, fac_jac, fac_adj, stream);
+}
+
+int vr_advect(const float* src, const int64_t dims[3], const float* disp, const float* factor, int order,
+              float* dst, int* nonfinite_flag, void* stream) {
+  return advect_impl(src, dims, -1, disp, factor, order, dst, nonfinite_flag, stream);
+}
+
+int vr_advect_slab(const float* src_ext, const int64_t dims[3], int xoff, const float* disp, const float* factor,
+                   int order, float* dst, int* nonfinite_flag, void* stream) {
+  if (xoff < 0) return VR_ERR_ARG;
+  return advect_impl(src_ext, dims, xoff, disp, factor, order, dst, nonfinite_flag, stream);
 }
 
 int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3], double dt, float* u0,
@@ -327,19 +399,14 @@ int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3]
 int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fwd, const float* vt,
                      const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
                      void* stream) {
-  Dims d;
-  int rc = dims_from(dims, &d);
-  if (rc) return rc;
-  if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  const dim3 g = vox_grid(d);
-  const int tpb = vox_tpb(d);
-  VR_DISPATCH_ORDER(order, {
-    incstate_step_kernel<ORD><<<g, tpb, 0, s>>>(u, d, disp_fwd, vt, gradm_next, (float)(0.5 * dt), last, out,
-                                                nonfinite_flag);
-  });
-  VR_CHECK_LAUNCH();
-  return VR_OK;
+  return incstate_impl(u, dims, -1, disp_fwd, vt, gradm_next, dt, order, last, out, nonfinite_flag, stream);
+}
+
+int vr_incstate_step_slab(const float* u_ext, const int64_t dims[3], int xoff, const float* disp_fwd,
+                          const float* vt, const float* gradm_next, double dt, int order, int last, float* out,
+                          int* nonfinite_flag, void* stream) {
+  if (xoff < 0) return VR_ERR_ARG;
+  return incstate_impl(u_ext, dims, xoff, disp_fwd, vt, gradm_next, dt, order, last, out, nonfinite_flag, stream);
 }
 
 int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
@@ -366,14 +433,39 @@ int vr_label_step(const float* src, const int* labels_in, int label_id, const in
   const bool from_l = labels_in != nullptr, to_l = labels_out != nullptr;
   VR_DISPATCH_ORDER(order, {
     if (from_l && to_l)
-      label_step_kernel<ORD, true, true><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, disp, nullptr,
-                                                           labels_out);
+      label_step_kernel<ORD, true, true, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, 0, disp, nullptr,
+                                                                  labels_out);
     else if (from_l)
-      label_step_kernel<ORD, true, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, true, false, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, 0, disp, dst,
+                                                                   nullptr);
     else if (to_l)
-      label_step_kernel<ORD, false, true><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, disp, nullptr, labels_out);
+      label_step_kernel<ORD, false, true, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, 0, disp, nullptr,
+                                                                   labels_out);
     else
-      label_step_kernel<ORD, false, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, false, false, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, 0, disp, dst,
+                                                                    nullptr);
+  });
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// slab label step from a float indicator / advected field with ghost planes
+int vr_label_step_slab(const float* src_ext, int label_id, const int64_t dims[3], int xoff, const float* disp,
+                       int order, float* dst, int* labels_out, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!src_ext || !disp || xoff < 0 || (!dst && !labels_out)) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 g = vox_grid(d);
+  const int tpb = vox_tpb(d);
+  VR_DISPATCH_ORDER(order, {
+    if (labels_out)
+      label_step_kernel<ORD, false, true, true><<<g, tpb, 0, s>>>(src_ext, nullptr, label_id, d, xoff, disp,
+                                                                  nullptr, labels_out);
+    else
+      label_step_kernel<ORD, false, false, true><<<g, tpb, 0, s>>>(src_ext, nullptr, label_id, d, xoff, disp, dst,
+                                                                   nullptr);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;

@@ -88,14 +88,89 @@ class SpectralWorkspace:
         return float(out.cpu()[0])
 
 
+class DistSpectralWorkspace:
+    """Spectral operators on x1 slabs (see csrc/spectral.cu "Distributed"):
+    local x3/x2 passes + pack -> one all-to-all per component -> x1 pass with
+    the symbol on complete x1 lines -> all-to-all back -> local x2/x3 inverse."""
+
+    def __init__(self, grid: Grid, ctx):
+        self.grid = grid
+        self.ctx = ctx
+        lib = _lib.lib()
+        n1, n2, n3 = grid.dims
+        self.n3h = n3 // 2 + 1
+        self._pl = C.c_void_p()
+        self._px = C.c_void_p()
+        _lib.check(lib.vr_spec_plan_create(_lib.dims_arg(ctx.local_dims), C.byref(self._pl)), "vr_spec_plan_create")
+        self._fin1 = weakref.finalize(self, _destroy_plan, self._pl)
+        _lib.check(lib.vr_spec_plan_create(_lib.dims_arg((n1, ctx.L2, n3)), C.byref(self._px)), "vr_spec_plan_create")
+        self._fin2 = weakref.finalize(self, _destroy_plan, self._px)
+        if not (lib.vr_spec_plan_is_fast(self._pl) and lib.vr_spec_plan_is_fast(self._px)):
+            raise NotImplementedError("distributed spectral operators need power-of-two N1/P, N2/P, N1, N2, N3/2")
+        nc = 3 * ctx.L1 * n2 * self.n3h          # complex elements per 3-component slab spectrum
+        dev = _lib.device()
+        self.send = torch.empty(2 * nc, dtype=torch.float64, device=dev)
+        self.recv = torch.empty(2 * nc, dtype=torch.float64, device=dev)
+        self.xout = torch.empty(2 * nc, dtype=torch.float32, device=dev)
+        self.irecv = torch.empty(2 * nc, dtype=torch.float32, device=dev)
+        self.per_comp = ctx.L1 * n2 * self.n3h   # complex elements per component
+        self.device = torch.cuda.current_device()
+
+    def _exchange(self, dst: torch.Tensor, src: torch.Tensor, ncomp: int, cplx_words: int) -> None:
+        m = self.per_comp * cplx_words
+        for c in range(ncomp):
+            self.ctx.alltoall(dst[c * m:(c + 1) * m], src[c * m:(c + 1) * m])
+
+    def apply(self, kind: int, x: torch.Tensor, out: torch.Tensor | None = None, add: torch.Tensor | None = None,
+              beta_v: float = 0.0, beta_w: float = 0.0, shift: float = 0.0, sigma: float = 0.0,
+              alpha: float = 1.0) -> torch.Tensor:
+        lib = _lib.lib()
+        st = _lib.stream()
+        ncomp = 3 if x.dim() == 4 else 1
+        if out is None:
+            out = torch.empty_like(x)
+        f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2)
+        P = self.ctx.world
+        _lib.check(lib.vr_dspec_forward(self._pl, x.data_ptr(), ncomp, int(f64), P, self.send.data_ptr(), st),
+                   "vr_dspec_forward")
+        snd = self.send if f64 else self.send.view(torch.float32)
+        rcv = self.recv if f64 else self.recv.view(torch.float32)
+        self._exchange(rcv, snd, ncomp, 2)
+        n1, n2, n3 = self.grid.dims
+        _lib.check(lib.vr_dspec_xpass(self._px, int(kind), ncomp, int(f64), float(beta_v), float(beta_w),
+                                      float(shift), float(sigma), float(alpha), n1 * n2 * n3,
+                                      self.ctx.rank * self.ctx.L2, n2, self.recv.data_ptr(), self.xout.data_ptr(),
+                                      st), "vr_dspec_xpass")
+        self._exchange(self.irecv, self.xout, ncomp, 2)
+        _lib.check(lib.vr_dspec_inverse(self._pl, self.irecv.data_ptr(), ncomp, P, _lib.ptr(add), out.data_ptr(),
+                                        st), "vr_dspec_inverse")
+        return out
+
+    def h1_energy(self, f: torch.Tensor) -> float:
+        lib = _lib.lib()
+        st = _lib.stream()
+        P = self.ctx.world
+        _lib.check(lib.vr_dspec_forward(self._pl, f.data_ptr(), 1, 1, P, self.send.data_ptr(), st),
+                   "vr_dspec_forward")
+        self._exchange(self.recv, self.send, 1, 2)
+        n = float(np.prod(self.grid.dims))
+        out = _lib.out_buf(1)
+        _lib.check(lib.vr_dspec_h1_partial(self._px, self.recv.data_ptr(), self.ctx.rank * self.ctx.L2,
+                                           self.grid.dims[1], TWO_PI ** 3 / (n * n), out.data_ptr(), st),
+                   "vr_dspec_h1_partial")
+        return float(self.ctx.allreduce(out.cpu().numpy(), "sum")[0])
+
+
 _ws_cache: dict = {}
 
 
-def workspace_for(grid: Grid) -> SpectralWorkspace:
-    key = (grid.dims, torch.cuda.current_device())
+def workspace_for(grid: Grid):
+    from . import dist
+    ctx = dist.current()
+    key = (grid.dims, torch.cuda.current_device(), id(ctx) if ctx is not None else None)
     ws = _ws_cache.get(key)
     if ws is None:
-        ws = SpectralWorkspace(grid)
+        ws = DistSpectralWorkspace(grid, ctx) if ctx is not None else SpectralWorkspace(grid)
         _ws_cache[key] = ws
     return ws
 
@@ -127,18 +202,32 @@ def _require_fd8(grid: Grid) -> None:
 
 # ---- FD8 (diffops.py:84-105) -------------------------------------------------
 def fd8_gradient_t(f: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    from . import dist
     dims = tuple(f.shape[-3:])
     if out is None:
         out = torch.empty((3,) + dims, dtype=torch.float32, device=f.device)
+    ctx = dist.current()
+    if ctx is not None:   # x1 slab: 4 ghost planes from the neighbours
+        ext = ctx.halo(f, 4)
+        _lib.check(_lib.lib().vr_fd8_grad_slab(ext.data_ptr(), _lib.dims_arg(dims), 4, ctx.dims[0],
+                                               out.data_ptr(), _lib.stream()), "vr_fd8_grad_slab")
+        return out
     _lib.check(_lib.lib().vr_fd8_grad(f.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
                "vr_fd8_grad")
     return out
 
 
 def fd8_divergence_t(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    from . import dist
     dims = tuple(v.shape[-3:])
     if out is None:
         out = torch.empty(dims, dtype=torch.float32, device=v.device)
+    ctx = dist.current()
+    if ctx is not None:
+        ext = ctx.halo(v, 4)
+        _lib.check(_lib.lib().vr_fd8_div_slab(ext.data_ptr(), _lib.dims_arg(dims), 4, ctx.dims[0], out.data_ptr(),
+                                              _lib.stream()), "vr_fd8_div_slab")
+        return out
     _lib.check(_lib.lib().vr_fd8_div(v.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
                "vr_fd8_div")
     return out

@@ -1,0 +1,127 @@
+"""x1-slab domain decomposition across the GPUs of one node.
+
+Rank r of P owns x1 planes [r*L1, (r+1)*L1), L1 = N1/P, of every voxel field
+(the paper's slab axis).  Three exchange steps exist, all issued
+through torch.distributed (NCCL on GPUs, gloo for the CPU tests of the host
+logic):
+
+* halo      -- ghost x1 planes for the FD8 stencil (4) and the semi-Lagrangian
+               gathers (ceil(max |x1 displacement|) + stencil, from an
+               allreduce-max of the velocity), one batched send/recv pair per
+               neighbour;
+* transpose -- one all-to-all per component before and after the x1 pass of
+               every spectral operator (x1 slabs <-> x2 slabs);
+* allreduce -- the f64 scalars of every reduction (dots, norms, extrema,
+               non-finite counts, Dice counts).
+
+`activate(ctx)` installs the context process-wide; the operator modules
+(diffops, transport, reductions, synth) consult `current()` and switch to the
+slab kernels, so optim.py's Gauss-Newton / PCG control flow runs unchanged.
+"""
+from __future__ import annotations
+
+import contextlib
+import math
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+_CTX = None
+
+
+def current():
+    return _CTX
+
+
+@contextlib.contextmanager
+def activate(ctx):
+    global _CTX
+    prev = _CTX
+    _CTX = ctx
+    try:
+        yield ctx
+    finally:
+        _CTX = prev
+
+
+class SlabContext:
+    """Decomposition of a global (N1, N2, N3) lattice into x1 slabs."""
+
+    def __init__(self, dims, group=None, rank: int | None = None, world: int | None = None):
+        self.dims = tuple(int(n) for n in dims)
+        self.group = group
+        self.rank = tdist.get_rank(group) if rank is None else rank
+        self.world = tdist.get_world_size(group) if world is None else world
+        n1, n2, n3 = self.dims
+        if n1 % self.world or n2 % self.world:
+            raise ValueError(f"N1={n1} and N2={n2} must be divisible by the number of ranks {self.world}")
+        self.L1 = n1 // self.world
+        self.L2 = n2 // self.world
+        self.x0 = self.rank * self.L1
+        self.local_dims = (self.L1, n2, n3)
+        self.left = (self.rank - 1) % self.world
+        self.right = (self.rank + 1) % self.world
+
+    # ---- collectives on small host arrays ---------------------------------------
+    def _dev(self):
+        return torch.device("cuda", torch.cuda.current_device()) if tdist.get_backend(self.group) == "nccl" \
+            else torch.device("cpu")
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
+        t = torch.as_tensor(np.asarray(values, dtype=np.float64).reshape(-1), device=self._dev())
+        rop = {"sum": tdist.ReduceOp.SUM, "max": tdist.ReduceOp.MAX, "min": tdist.ReduceOp.MIN}[op]
+        tdist.all_reduce(t, op=rop, group=self.group)
+        return t.cpu().numpy()
+
+    # ---- ghost planes --------------------------------------------------------------
+    def halo(self, x: torch.Tensor, w: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """(..., L1, N2, N3) local slab -> (..., L1 + 2w, N2, N3) with w periodic
+        ghost planes on each side taken from the x1 neighbours."""
+        L1 = x.shape[-3]
+        if w > L1:
+            raise ValueError(f"ghost width {w} exceeds the slab depth {L1}; use fewer ranks")
+        shape = tuple(x.shape[:-3]) + (L1 + 2 * w,) + tuple(x.shape[-2:])
+        ext = out if out is not None else torch.empty(shape, dtype=x.dtype, device=x.device)
+        ext[..., w:w + L1, :, :].copy_(x)
+        if w == 0:
+            return ext
+        if self.world == 1:
+            ext[..., :w, :, :].copy_(x[..., L1 - w:, :, :])
+            ext[..., w + L1:, :, :].copy_(x[..., :w, :, :])
+            return ext
+        send_lo = x[..., :w, :, :].contiguous()          # -> left neighbour's right ghost
+        send_hi = x[..., L1 - w:, :, :].contiguous()     # -> right neighbour's left ghost
+        recv_hi = torch.empty_like(send_lo)              # <- right neighbour's first planes
+        recv_lo = torch.empty_like(send_hi)              # <- left neighbour's last planes
+        ops = [tdist.P2POp(tdist.isend, send_lo, self.left, self.group),
+               tdist.P2POp(tdist.isend, send_hi, self.right, self.group),
+               tdist.P2POp(tdist.irecv, recv_hi, self.right, self.group),
+               tdist.P2POp(tdist.irecv, recv_lo, self.left, self.group)]
+        for req in tdist.batch_isend_irecv(ops):
+            req.wait()
+        ext[..., :w, :, :].copy_(recv_lo)
+        ext[..., w + L1:, :, :].copy_(recv_hi)
+        return ext
+
+    # ---- transposes -------------------------------------------------------------
+    def alltoall(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        """Equal-split all-to-all along dim 0 of flat views (x1 slabs <-> x2 slabs)."""
+        if self.world == 1:
+            out.copy_(inp)
+            return
+        tdist.all_to_all_single(out, inp, group=self.group)
+
+    # ---- synthetic-input helpers -------------------------------------------------
+    def local_coords(self) -> np.ndarray:
+        """(3, L1, N2, N3) lattice coordinates of this rank's planes."""
+        n1, n2, n3 = self.dims
+        ax = [np.arange(self.x0, self.x0 + self.L1) * (2 * np.pi / n1), np.arange(n2) * (2 * np.pi / n2),
+              np.arange(n3) * (2 * np.pi / n3)]
+        return np.stack(np.meshgrid(*ax, indexing="ij"))
+
+
+def ghost_width(vmax1: float, dt: float, n1: int, order: str) -> int:
+    """x1 ghost planes covering every departure point plus the stencil."""
+    h1 = 2 * math.pi / n1
+    return max(4, int(math.ceil(dt * vmax1 / h1)) + (3 if order == "cubic" else 2))

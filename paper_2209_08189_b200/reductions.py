@@ -8,10 +8,17 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import dist as _dist
 
 
 def _n(t: torch.Tensor) -> int:
     return t.numel()
+
+
+def _sum(x: np.ndarray) -> np.ndarray:
+    """Cross-rank sum of partial results when a slab decomposition is active."""
+    ctx = _dist.current()
+    return x if ctx is None else ctx.allreduce(x, "sum")
 
 
 def dots(pairs) -> np.ndarray:
@@ -24,7 +31,7 @@ def dots(pairs) -> np.ndarray:
     a = _lib.ptr_array([p[0] for p in pairs])
     b = _lib.ptr_array([p[1] for p in pairs])
     _lib.check(lib.vr_dots(k, a, b, n, _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()), "vr_dots")
-    return out.cpu().numpy()
+    return _sum(out.cpu().numpy())
 
 
 def dot(a: torch.Tensor, b: torch.Tensor) -> float:
@@ -36,7 +43,7 @@ def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> n
     out = _lib.out_buf(2)
     _lib.check(lib.vr_sqdiff(a.data_ptr(), b.data_ptr(), _lib.ptr(c), _n(a), _lib.scratch().data_ptr(),
                              out.data_ptr(), _lib.stream()), "vr_sqdiff")
-    return out.cpu().numpy()
+    return _sum(out.cpu().numpy())
 
 
 def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
@@ -44,6 +51,25 @@ def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
     out = _lib.out_buf(4)
     _lib.check(lib.vr_minmax(a.data_ptr(), _lib.ptr(b), _n(a), _lib.scratch().data_ptr(), out.data_ptr(),
                              _lib.stream()), "vr_minmax")
+    o = out.cpu().numpy()
+    ctx = _dist.current()
+    if ctx is not None:
+        m = ctx.allreduce(np.array([-o[0], o[1], -o[2], o[3]]), "max")
+        o = np.array([-m[0], m[1], -m[2], m[3]])
+    return o
+
+
+def local_absmax(x: torch.Tensor) -> float:
+    """max |x| over this rank's data (host-side sizing of ghost widths)."""
+    mn, mx, _, _ = minmax_local(x)
+    return max(abs(mn), abs(mx))
+
+
+def minmax_local(a: torch.Tensor) -> np.ndarray:
+    lib = _lib.lib()
+    out = _lib.out_buf(4)
+    _lib.check(lib.vr_minmax(a.data_ptr(), None, _n(a), _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()),
+               "vr_minmax")
     return out.cpu().numpy()
 
 
@@ -54,6 +80,11 @@ def vecstats(v: torch.Tensor) -> tuple:
     _lib.check(lib.vr_vecstats(v.data_ptr(), _n(v) // 3, _lib.scratch().data_ptr(), out.data_ptr(),
                                _lib.stream()), "vr_vecstats")
     o = out.cpu().numpy()
+    ctx = _dist.current()
+    if ctx is not None:
+        mx = ctx.allreduce(o[1:2], "max")[0]
+        cnt = ctx.allreduce(o[2:4], "sum")
+        o = np.array([o[0], mx, cnt[0], cnt[1]])
     return float(o[1]), int(o[2]), int(o[3])
 
 
@@ -79,9 +110,15 @@ def fill(out: torch.Tensor, value: float) -> torch.Tensor:
 
 def label_histogram(l0: torch.Tensor, l1: torch.Tensor, max_id: int | None = None) -> np.ndarray:
     """counts[id] = (|l0==id|, |l1==id|, |l0==id & l1==id|) as exact int64."""
+    ctx = _dist.current()
     if max_id is None:
         max_id = int(max(int(l0.max()), int(l1.max()))) if l0.numel() else 0
+        if ctx is not None:
+            max_id = int(ctx.allreduce([max_id], "max")[0])
     counts = torch.empty(3 * (max_id + 1), dtype=torch.int64, device=l0.device)
     _lib.check(_lib.lib().vr_label_counts(l0.data_ptr(), l1.data_ptr(), _n(l0), int(max_id), counts.data_ptr(),
                                           _lib.stream()), "vr_label_counts")
-    return counts.cpu().numpy().reshape(max_id + 1, 3)
+    c = counts.cpu().numpy().reshape(max_id + 1, 3)
+    if ctx is not None:
+        c = np.rint(ctx.allreduce(c.reshape(-1).astype(np.float64), "sum")).astype(np.int64).reshape(max_id + 1, 3)
+    return c

@@ -25,13 +25,23 @@ def make_velocity(K: int, grid: Grid) -> VectorField:
     return VectorField(grid, velocity_array(K, grid))
 
 
+def _coords(grid: Grid) -> np.ndarray:
+    """Lattice coordinates of this rank's part of `grid` (all of it unless an
+    x1-slab decomposition is active)."""
+    from . import dist
+    ctx = dist.current()
+    if ctx is not None and tuple(ctx.dims) == tuple(grid.dims):
+        return ctx.local_coords()
+    return grid.coords()
+
+
 def velocity_array(K: int, grid: Grid) -> np.ndarray:
     if K < 1:
         raise ValueError("K must be >= 1")
-    x, y, z = grid.coords() - math.pi
-    vx = np.zeros(grid.dims)
-    vy = np.zeros(grid.dims)
-    vz = np.zeros(grid.dims)
+    x, y, z = _coords(grid) - math.pi
+    vx = np.zeros(x.shape)
+    vy = np.zeros(x.shape)
+    vz = np.zeros(x.shape)
     for k in range(1, K + 1):
         a = k ** -0.5
         vx += a * np.cos(k * y) * np.cos(k * x)
@@ -46,13 +56,24 @@ def transport_labels(labels: LabelMap, v: VectorField, cfg: TransportConfig,
     0.5; overlap ties go to the larger label id (synth.py:121-131)."""
     ops = ops or TransportOperators(v, cfg)
     lib = _lib.lib()
-    dims = labels.grid.dims
+    dims = tuple(labels.labels.shape)
     d = _lib.dims_arg(dims)
     st = _lib.stream()
     order = _lib.ORDER[cfg.interp_order]
     disp = ops.forward.displacement.data_ptr()
     out = torch.zeros(dims, dtype=torch.int32, device=labels.labels.device)
     bufs = [torch.empty(dims, dtype=torch.float32, device=out.device) for _ in range(2)]
+    if ops.ctx is not None:   # x1 slabs: float indicator + halo'd sweeps
+        for lab in labels.label_ids():
+            cur = (labels.labels == lab).to(torch.float32)
+            for j in range(cfg.n_t):
+                if j < cfg.n_t - 1:
+                    cur = ops.sweep(cur, ops.forward.displacement, out=bufs[j % 2])
+                else:
+                    ext = ops.ctx.halo(cur, ops.w)
+                    _lib.check(lib.vr_label_step_slab(ext.data_ptr(), int(lab), d, ops.w, disp, order, None,
+                                                      out.data_ptr(), st), "vr_label_step_slab")
+        return LabelMap(labels.grid, out)
     for lab in labels.label_ids():
         src = None
         for j in range(cfg.n_t):
@@ -74,7 +95,7 @@ def make_reference(m0: ScalarField, labels: LabelMap, v: VectorField, cfg: Trans
 
 # ---- benchmark problems ---------------------------------------
 def _gauss(grid: Grid, c, s) -> np.ndarray:
-    x = grid.coords()
+    x = _coords(grid)
     d2 = sum((x[i] - c[i]) ** 2 for i in range(3))
     return np.exp(-d2 / (2 * s * s))
 
@@ -98,7 +119,7 @@ def c1_problem(grid: Grid, order: str = "cubic"):
 
 def sphere_template(grid: Grid, radius: float = 1.2, width: float = 0.19635):
     """C2 template: smoothed ball (float32) and its label map (int32)."""
-    x = grid.coords()
+    x = _coords(grid)
     r = np.sqrt(sum((x[i] - math.pi) ** 2 for i in range(3)))
     m0 = (0.5 * (1.0 - np.tanh((r - radius) / width))).astype(np.float32)
     return m0, (r <= radius).astype(np.int32)

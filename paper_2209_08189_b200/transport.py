@@ -12,9 +12,12 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import torch
 
 from . import _lib
+from . import dist as _dist
 from .diffops import fd8_divergence_t, fd8_gradient_t
 from .errors import TransportError
 from .grid import Grid, ScalarField, VectorField, TWO_PI
@@ -126,18 +129,81 @@ class TransportOperators:
         self.v = v
         self.cfg = cfg
         self.grid = v.grid
-        self.div = fd8_divergence_t(v.data)
-        disp_f, disp_b, self.jac_factor, self.adj_factor = _trace(v.data, v.grid.dims, cfg.dt, cfg.interp_order,
-                                                                  self.div)
+        ctx = _dist.current()
+        self.ctx = ctx if ctx is not None and tuple(ctx.dims) == tuple(v.grid.dims) else None
+        if self.ctx is None:
+            self.div = fd8_divergence_t(v.data)
+            disp_f, disp_b, self.jac_factor, self.adj_factor = _trace(v.data, v.grid.dims, cfg.dt, cfg.interp_order,
+                                                                      self.div)
+        else:
+            disp_f, disp_b = self._trace_slab(v.data)
         self.forward = Characteristics(v.grid, disp_f, cfg.dt)
         self.backward = Characteristics(v.grid, disp_b, cfg.dt)
         self.flag = torch.zeros(1, dtype=torch.int32, device=v.data.device)
 
+    # ---- x1-slab decomposition (dist.py) ----------------------------------------
+    def _trace_slab(self, v: torch.Tensor):
+        """Ghost width from the global max |v1| (allreduce), one halo exchange
+        of v (covers both the FD8 divergence and the RK2 star points), one of
+        div (for the source factors), then the slab trace kernel."""
+        from .reductions import local_absmax
+        ctx, cfg = self.ctx, self.cfg
+        vmax1 = float(ctx.allreduce([local_absmax(v[0])], "max")[0])
+        self.w = _dist.ghost_width(vmax1, cfg.dt, self.grid.dims[0], cfg.interp_order)
+        ldims = ctx.local_dims
+        v_ext = ctx.halo(v, self.w)
+        self.div = torch.empty(ldims, dtype=torch.float32, device=v.device)
+        lib = _lib.lib()
+        st = _lib.stream()
+        _lib.check(lib.vr_fd8_div_slab(v_ext.data_ptr(), _lib.dims_arg(ldims), self.w, ctx.dims[0],
+                                       self.div.data_ptr(), st), "vr_fd8_div_slab")
+        div_ext = ctx.halo(self.div, self.w)
+        disp_f = torch.empty_like(v)
+        disp_b = torch.empty_like(v)
+        self.jac_factor = torch.empty_like(self.div)
+        self.adj_factor = torch.empty_like(self.div)
+        dims4 = (C.c_int64 * 4)(*ldims, ctx.dims[0])
+        _lib.check(lib.vr_trace_rk2_slab(v_ext.data_ptr(), dims4, self.w, float(cfg.dt), _order(cfg.interp_order),
+                                         disp_f.data_ptr(), disp_b.data_ptr(), div_ext.data_ptr(),
+                                         self.jac_factor.data_ptr(), self.adj_factor.data_ptr(), st),
+                   "vr_trace_rk2_slab")
+        return disp_f, disp_b
+
+    def sweep(self, values: torch.Tensor, disp: torch.Tensor, factor: torch.Tensor | None = None,
+              out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
+        """One SL step dst = interp(values, departure) [* factor] (halo'd on slabs)."""
+        if self.ctx is None:
+            return advect(values, disp, self.cfg.interp_order, factor=factor, out=out, flag=flag)
+        if out is None:
+            out = torch.empty(values.shape, dtype=torch.float32, device=values.device)
+        ext = self.ctx.halo(values, self.w)
+        _lib.check(_lib.lib().vr_advect_slab(ext.data_ptr(), _lib.dims_arg(self.ctx.local_dims), self.w,
+                                             disp.data_ptr(), _lib.ptr(factor), _order(self.cfg.interp_order),
+                                             out.data_ptr(), _lib.ptr(flag), _lib.stream()), "vr_advect_slab")
+        return out
+
+    def inc_step(self, u: torch.Tensor, vt: torch.Tensor, gnext: torch.Tensor, last: int, out: torch.Tensor,
+                 flag=None) -> None:
+        """Incremental-state step (transport.py:174-183) along the forward trace."""
+        lib = _lib.lib()
+        cfg = self.cfg
+        dims = _lib.dims_arg(u.shape[-3:])
+        disp = self.forward.displacement.data_ptr()
+        if self.ctx is None:
+            rc = lib.vr_incstate_step(u.data_ptr(), dims, disp, vt.data_ptr(), gnext.data_ptr(), float(cfg.dt),
+                                      _order(cfg.interp_order), last, out.data_ptr(), _lib.ptr(flag), _lib.stream())
+        else:
+            ext = self.ctx.halo(u, self.w)
+            rc = lib.vr_incstate_step_slab(ext.data_ptr(), dims, self.w, disp, vt.data_ptr(), gnext.data_ptr(),
+                                           float(cfg.dt), _order(cfg.interp_order), last, out.data_ptr(),
+                                           _lib.ptr(flag), _lib.stream())
+        _lib.check(rc, "vr_incstate_step")
+
     def advect_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
-        return advect(values, self.forward.displacement, self.cfg.interp_order, out=out, flag=flag)
+        return self.sweep(values, self.forward.displacement, out=out, flag=flag)
 
     def advect_back_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
-        return advect(values, self.backward.displacement, self.cfg.interp_order, out=out, flag=flag)
+        return self.sweep(values, self.backward.displacement, out=out, flag=flag)
 
     # non-finite guard (transport.py:119-121) read back at the reference's check points
     def arm(self) -> torch.Tensor:
@@ -160,7 +226,7 @@ def solve_state_series(m0: ScalarField, v: VectorField, cfg: TransportConfig,
     if m0.grid != v.grid:
         raise TransportError("template and velocity grids differ")
     ops = _ops_for(v, cfg, ops)
-    series = torch.empty((cfg.n_t + 1,) + m0.grid.dims, dtype=torch.float32, device=m0.values.device)
+    series = torch.empty((cfg.n_t + 1,) + tuple(m0.values.shape), dtype=torch.float32, device=m0.values.device)
     series[0].copy_(m0.values)
     flag = ops.arm()
     for j in range(cfg.n_t):
@@ -194,7 +260,8 @@ def solve_adjoint(final_lambda: ScalarField, v: VectorField, cfg: TransportConfi
     if final_lambda.grid != v.grid:
         raise TransportError("adjoint final condition and velocity grids differ")
     ops = _ops_for(v, cfg, ops)
-    series = torch.empty((cfg.n_t + 1,) + v.grid.dims, dtype=torch.float32, device=v.data.device)
+    series = torch.empty((cfg.n_t + 1,) + tuple(final_lambda.values.shape), dtype=torch.float32,
+                         device=v.data.device)
     series[cfg.n_t].copy_(final_lambda.values)
     _adjoint_sweep(series, ops, cfg)
     return series
@@ -203,8 +270,8 @@ def solve_adjoint(final_lambda: ScalarField, v: VectorField, cfg: TransportConfi
 def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: TransportConfig) -> None:
     flag = ops.arm()
     for j in range(cfg.n_t - 1, -1, -1):
-        advect(series[j + 1], ops.backward.displacement, cfg.interp_order, factor=ops.adj_factor, out=series[j],
-               flag=flag if j == 0 else None)
+        ops.sweep(series[j + 1], ops.backward.displacement, factor=ops.adj_factor, out=series[j],
+                  flag=flag if j == 0 else None)
     ops.raise_if_flagged("adjoint solve")
 
 
@@ -220,7 +287,7 @@ def gradient_series(m_series: torch.Tensor) -> torch.Tensor:
 def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOperators, cfg: TransportConfig,
                  last_mode: int, out: torch.Tensor | None = None) -> torch.Tensor:
     lib = _lib.lib()
-    dims = ops.grid.dims
+    dims = tuple(vt.shape[-3:])
     d = _lib.dims_arg(dims)
     st = _lib.stream()
     u = torch.empty(dims, dtype=torch.float32, device=vt.device)
@@ -228,14 +295,10 @@ def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOp
                "vr_incstate_init")
     other = torch.empty_like(u)
     flag = ops.arm()
-    order = _order(cfg.interp_order)
     for j in range(cfg.n_t):
         last = j == cfg.n_t - 1
         dst = out if (last and out is not None) else other
-        rc = lib.vr_incstate_step(u.data_ptr(), d, ops.forward.displacement.data_ptr(), vt.data_ptr(),
-                                  grad_m_series[j + 1].data_ptr(), float(cfg.dt), order, last_mode if last else 0,
-                                  dst.data_ptr(), _lib.ptr(flag) if last else None, st)
-        _lib.check(rc, "vr_incstate_step")
+        ops.inc_step(u, vt, grad_m_series[j + 1], last_mode if last else 0, dst, flag if last else None)
         if not last:
             u, other = dst, u
         else:
@@ -258,14 +321,14 @@ def jacobian_determinant(v: VectorField, cfg: TransportConfig, ops: TransportOpe
     """det of the deformation gradient at t = 1 via dJ/dt + v.grad(J) = J div(v),
     J(0) = 1 (transport.py:188-197)."""
     ops = _ops_for(v, cfg, ops)
-    cur = torch.empty(v.grid.dims, dtype=torch.float32, device=v.data.device)
+    cur = torch.empty(tuple(v.data.shape[1:]), dtype=torch.float32, device=v.data.device)
     from .reductions import fill
     fill(cur, 1.0)
     other = torch.empty_like(cur)
     flag = ops.arm()
     for j in range(cfg.n_t):
-        advect(cur, ops.forward.displacement, cfg.interp_order, factor=ops.jac_factor, out=other,
-               flag=flag if j == cfg.n_t - 1 else None)
+        ops.sweep(cur, ops.forward.displacement, factor=ops.jac_factor, out=other,
+                  flag=flag if j == cfg.n_t - 1 else None)
         cur, other = other, cur
     ops.raise_if_flagged("Jacobian-determinant solve")
     return ScalarField(v.grid, cur)
