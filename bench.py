@@ -8,8 +8,11 @@ cubic, n_t=4, beta_v=1e-2, beta_w=0, GN-PCG to gtol 5e-2; one step = one full
 `register()` call from pinned host buffers incl. label transport + Dice and
 the velocity/deformed-image read-back (e2e).  Synthetic data.
 
-N > 1 (this round): independent replicas of the same registration on every
-rank ("weak", no data-path collective yet), max-over-ranks device time.
+N > 1: the SAME registration decomposed into x1 slabs over N GPUs (strong
+scaling; dist.py: NCCL halo exchange for the SL / FD8 stencils, all-to-all
+transposes for the spectral operators, allreduce of the PCG/GN scalars),
+max-over-ranks device time.  --n / --order / --nt / --beta-w select other
+sizes, e.g. the C3 shape `--n 1024 --order linear --nt 16 --beta-w 1e-4`.
 
 --impl reference: the CPU oracle (oracle/velreg_oracle.py, numpy + numba, all
 host threads) on a bounded sample of the same workload (one objective
@@ -45,6 +48,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--order", default="cubic", choices=["cubic", "linear"])
+    ap.add_argument("--nt", type=int, default=4)
+    ap.add_argument("--beta-w", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     return ap.parse_args()
@@ -211,10 +217,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    from paper_2209_08189_b200 import dist as pdist
     n = args.n
     g = P.make_grid((n, n, n))
-    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=0.0, n_t=4, interp_order="cubic")
-    m0, m1, l0, l1, _ = c2_problem(g)
+    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=args.beta_w, n_t=args.nt, interp_order=args.order)
+    slab = pdist.SlabContext(g.dims) if ws > 1 else None
+    act = pdist.activate(slab)
+    act.__enter__()
+    m0, m1, l0, l1, _ = c2_problem(g, args.order, args.nt)
     l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
 
     def one():
@@ -227,7 +237,12 @@ def run_ours(args):
     # ---- timed region: device-resident inputs ---------------------------------
     stream = torch.cuda.current_stream()
     dominant = "vr_advect"
-    _lib.PROFILE.reset(timed=(dominant, "vr_spec_apply", "vr_trace_rk2", "vr_fd8_grad"))
+    if ws > 1:
+        dominant = "vr_advect_slab"
+    _lib.PROFILE.reset(timed=(dominant, "vr_spec_apply", "vr_trace_rk2", "vr_fd8_grad", "vr_trace_rk2_slab",
+                              "vr_dspec_forward", "vr_dspec_xpass", "vr_dspec_inverse", "vr_fd8_grad_slab",
+                              "vr_incstate_step_slab", "vr_incstate_step", "vr_body_force", "dist.ghosts",
+                              "dist.alltoall", "dist.allreduce"))
     clocks = ClockSampler(local)
     times = []
     barrier()
@@ -250,7 +265,7 @@ def run_ours(args):
     launches = _lib.PROFILE.total_launches()
     kern = {name: _lib.PROFILE.avg_ms(name) for name in _lib.PROFILE.timed}
     t_step = max_over_ranks(sum(times) / len(times))
-    value = t_step / ws   # whole-job seconds per registration (replicas)
+    value = t_step   # seconds per registration of the whole job (max over ranks)
 
     # ---- e2e through the public API from pinned host buffers -------------------
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
@@ -258,8 +273,8 @@ def run_ours(args):
     h_m1 = torch.from_numpy(m1.numpy()).pin_memory()
     h_l0 = torch.from_numpy(l0.numpy()).pin_memory()
     h_l1 = torch.from_numpy(l1.numpy()).pin_memory()
-    h_v = torch.empty((3, n, n, n), dtype=torch.float32).pin_memory()
-    h_def = torch.empty((n, n, n), dtype=torch.float32).pin_memory()
+    h_v = torch.empty((3,) + tuple(m0.values.shape), dtype=torch.float32).pin_memory()
+    h_def = torch.empty(tuple(m0.values.shape), dtype=torch.float32).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in (h_m0, h_m1, h_l0, h_l1))
     d2h = h_v.numel() * 4 + h_def.numel() * 4 + 8
     e2e_times = []
@@ -282,13 +297,14 @@ def run_ours(args):
         b.synchronize()
         dice = res.dice.d_a
         e2e_times.append(a.elapsed_time(b) / 1e3)
-    e2e_val = max_over_ranks(sum(e2e_times) / len(e2e_times)) / ws
+    e2e_val = max_over_ranks(sum(e2e_times) / len(e2e_times))
 
     # ---- roofline of the dominant kernel -------------------------------------
     peaks = measured_peaks()
     per_unit = 20.0  # B per interpolated point: 12 B characteristic + 4 B out + 4 B source
     avg_ms, nlaunch = kern.get(dominant, (0.0, 0))
-    achieved = (per_unit * g.num_voxels / (avg_ms * 1e-3) / 1e9) if avg_ms > 0 else None
+    units = g.num_voxels // ws   # points per launch on this rank
+    achieved = (per_unit * units / (avg_ms * 1e-3) / 1e9) if avg_ms > 0 else None
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
@@ -297,7 +313,7 @@ def run_ours(args):
     step_ms = t_step * 1e3
     kernels = {k: {"avg_ms": round(v[0], 5), "launches_per_step": v[1] // max(args.steps, 1),
                    "share_of_step": round(v[0] * v[1] / max(args.steps, 1) / step_ms, 4)}
-               for k, v in kern.items()}
+               for k, v in kern.items() if v[1] > 0}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -307,19 +323,20 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (f64 reductions / forward spectra)", "data": "synthetic",
-            "config": {"workload": f"C2 sphere->deformed sphere {n}^3 GN-PCG, cubic, n_t=4, beta_v=1e-2, "
-                                   f"beta_w=0, gtol=5e-2", "parallelism": "replicas" if ws > 1 else "single",
+            "config": {"workload": f"C2 sphere->deformed sphere {n}^3 GN-PCG, {args.order}, n_t={args.nt}, "
+                                   f"beta_v=1e-2, beta_w={args.beta_w:g}, gtol=5e-2",
+                       "parallelism": f"x1-slab x{ws} (NCCL halo / all-to-all / allreduce)" if ws > 1 else "single",
                        "l2": "256 MB buffer written between timed steps; working set > 126 MB L2",
                        "gn_iterations": diag.gn_iterations,
                        "pcg": [r.pcg_iterations for r in diag.iterations],
                        "matvecs": diag.matvecs, "relative_residual": diag.relative_residual,
                        "launches_per_step": launches // max(args.steps, 1),
                        "dice_post": dice},
-            "e2e": {"value": e2e_val, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_val, "unit": "s", "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "advect_kernel<cubic> (vr_advect)",
+            "roofline": {"bound": "hbm", "kernel": f"advect_kernel<{args.order}> ({dominant})",
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
                          "peak_source": peaks["source"], "bytes_per_unit": per_unit,
@@ -329,6 +346,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    act.__exit__(None, None, None)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -140,25 +140,33 @@ int vr_label_counts(const int* l0, const int* l1, int64_t n, int max_id, unsigne
                     void* stream);
 
 /* ---- x1-slab (multi-GPU) variants ---------------------------------------------
- * A rank owns x1 planes [r*L1, (r+1)*L1) of every field.  `*_ext` inputs carry
- * `xoff` ghost planes on each side (filled by the host's NCCL halo exchange,
- * paper_2209_08189_b200/dist.py); dims are the LOCAL (L1, N2, N3); outputs are
- * local.  The ghost width must cover the largest x1 displacement plus the
- * stencil (the host sizes it from an allreduce-max). */
-int vr_trace_rk2_slab(const float* v_ext, const int64_t dims4[4] /* L1,N2,N3,N1 */, int xoff, double dt, int order,
+ * A rank owns x1 planes [r*L1, (r+1)*L1) of every field.  A gathered source is
+ * passed as its local slab plus two ghost blocks of w planes each: `*_lo` holds
+ * the w planes before the slab, `*_hi` the w planes after it (filled by the
+ * host's NCCL halo exchange, paper_2209_08189_b200/dist.py; vector sources have
+ * ghost blocks of shape (3, w, N2, N3)).  dims are the LOCAL (L1, N2, N3);
+ * outputs are local.  w must cover the largest x1 displacement plus the stencil
+ * (the host sizes it from an allreduce-max of the velocity). */
+/* trace on a slab: v_ext (3, L1+2w, N2, N3) and div_ext (L1+2w, N2, N3) are
+ * contiguous ghost-extended copies (built once per velocity iterate) */
+int vr_trace_rk2_slab(const float* v_ext, const int64_t dims[3], int64_t n1_global, int w, double dt, int order,
                       float* disp_fwd, float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj,
                       void* stream);
-int vr_advect_slab(const float* src_ext, const int64_t dims[3], int xoff, const float* disp, const float* factor,
-                   int order, float* dst, int* nonfinite_flag, void* stream);
-int vr_incstate_step_slab(const float* u_ext, const int64_t dims[3], int xoff, const float* disp_fwd,
-                          const float* vt, const float* gradm_next, double dt, int order, int last, float* out,
-                          int* nonfinite_flag, void* stream);
-int vr_label_step_slab(const float* src_ext, int label_id, const int64_t dims[3], int xoff, const float* disp,
-                       int order, float* dst, int* labels_out, void* stream);
-int vr_fd8_grad_slab(const float* f_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out3,
-                     void* stream);
-int vr_fd8_div_slab(const float* v3_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out,
-                    void* stream);
+int vr_advect_slab(const float* src, const float* src_lo, const float* src_hi, const int64_t dims[3], int w,
+                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag,
+                   void* stream);
+int vr_incstate_step_slab(const float* u, const float* u_lo, const float* u_hi, const int64_t dims[3], int w,
+                          const float* disp_fwd, const float* vt, const float* gradm_next, double dt, int order,
+                          int last, float* out, int* nonfinite_flag, void* stream);
+int vr_label_step_slab(const float* src, const float* src_lo, const float* src_hi, int label_id,
+                       const int64_t dims[3], int w, const float* disp, int order, float* dst, int* labels_out,
+                       void* stream);
+/* FD8 on a slab: ghost blocks of exactly 4 planes (component 0 only for the
+ * divergence: x1 derivatives are taken of v1 alone) */
+int vr_fd8_grad_slab(const float* f, const float* f_lo, const float* f_hi, const int64_t dims[3], int64_t n1_global,
+                     float* out3, void* stream);
+int vr_fd8_div_slab(const float* v3, const float* v1_lo, const float* v1_hi, const int64_t dims[3],
+                    int64_t n1_global, float* out, void* stream);
 
 /* distributed spectral operator = forward (x3, x2 local + pack) -> host
  * all-to-all per component -> X pass on x1 lines -> host all-to-all back ->

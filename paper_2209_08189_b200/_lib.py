@@ -55,12 +55,12 @@ _SIGS = {
     "vr_fill": [_i64, _f32, _p, _p],
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
     # x1-slab / distributed
-    "vr_trace_rk2_slab": [_p, _dims_t, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
-    "vr_advect_slab": [_p, _dims_t, _i32, _p, _p, _i32, _p, _p, _p],
-    "vr_incstate_step_slab": [_p, _dims_t, _i32, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
-    "vr_label_step_slab": [_p, _i32, _dims_t, _i32, _p, _i32, _p, _p, _p],
-    "vr_fd8_grad_slab": [_p, _dims_t, _i32, _i64, _p, _p],
-    "vr_fd8_div_slab": [_p, _dims_t, _i32, _i64, _p, _p],
+    "vr_trace_rk2_slab": [_p, _dims_t, _i64, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
+    "vr_advect_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _i32, _p, _p, _p],
+    "vr_incstate_step_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
+    "vr_label_step_slab": [_p, _p, _p, _i32, _dims_t, _i32, _p, _i32, _p, _p, _p],
+    "vr_fd8_grad_slab": [_p, _p, _p, _dims_t, _i64, _p, _p],
+    "vr_fd8_div_slab": [_p, _p, _p, _dims_t, _i64, _p, _p],
     "vr_spec_plan_is_fast": [_p],
     "vr_dspec_forward": [_p, _p, _i32, _i32, _i32, _p, _p],
     "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _p, _p, _p],
@@ -118,6 +118,28 @@ class Profile:
 
 
 PROFILE = Profile()
+
+
+class timed:
+    """CUDA-event bracket of a host-orchestrated phase (e.g. a halo exchange),
+    recorded under `name` when PROFILE is enabled and `name` is timed."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.on = PROFILE.enabled and name in PROFILE.timed
+
+    def __enter__(self):
+        if self.on:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.a.record(torch.cuda.current_stream())
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record(torch.cuda.current_stream())
+            PROFILE.events[self.name].append((self.a, b))
+        return False
 
 
 class _Bound:

@@ -46,13 +46,16 @@ __device__ __forceinline__ void load_tile(float (*tile)[TZ + 2 * HALO + 1], cons
 // MODE 0: gradient of a scalar (3 outputs); MODE 1: divergence of a vector.
 // SLAB: the input is an x1 slab with `xoff` (>= 4) ghost planes per side and
 // component stride `cs`; d = local (output) dims, no x1 wrap.
+// SLAB: the x1 window reads ghost planes from lo (4 planes before the slab) /
+// hi (4 planes after); y/z tiles only ever read the local plane.
 template <int MODE, bool SLAB>
-__global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f, Dims d, int xoff, int64_t cs,
-                                                     float h1, float h2, float h3, float* __restrict__ out,
-                                                     int nx) {
+__global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f, const float* __restrict__ lo,
+                                                     const float* __restrict__ hi, Dims d, float h1, float h2,
+                                                     float h3, float* __restrict__ out, int nx) {
   __shared__ float tile[TY + 2 * HALO][TZ + 2 * HALO + 1];
   const int64_t N = d.n();
-  const int sx = SLAB ? xoff : 0;   // source plane = output plane + sx
+  const int64_t cs = N;
+  const int psz = d.n2 * d.n3;
   const int k0 = blockIdx.x * TZ, j0 = blockIdx.y * TY;
   const int i_begin = blockIdx.z * nx;
   const int i_end = min(i_begin + nx, d.n1);
@@ -64,16 +67,29 @@ __global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f
   if (active) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
-      int ii = i_begin - HALO + o + sx;
-      if (!SLAB) ii = ii < 0 ? ii + d.n1 : (ii >= d.n1 ? ii - d.n1 : ii);  // n1 >= 9 (caller)
-      w[o] = __ldg(fx + ((int64_t)ii * d.n2 + j) * d.n3 + k);
+      int ii = i_begin - HALO + o;
+      const float* pl;
+      if (SLAB) {
+        pl = ii < 0 ? lo + (int64_t)(ii + HALO) * psz : (ii >= d.n1 ? hi + (int64_t)(ii - d.n1) * psz
+                                                                    : fx + (int64_t)ii * psz);
+      } else {
+        ii = ii < 0 ? ii + d.n1 : (ii >= d.n1 ? ii - d.n1 : ii);  // n1 >= 9 (caller)
+        pl = fx + (int64_t)ii * psz;
+      }
+      w[o] = __ldg(pl + j * d.n3 + k);
     }
   }
   for (int i = i_begin; i < i_end; ++i) {
     if (active) {
-      int ii = i + HALO + sx;
-      if (!SLAB) ii = ii >= d.n1 ? ii - d.n1 : ii;
-      w[8] = __ldg(fx + ((int64_t)ii * d.n2 + j) * d.n3 + k);
+      int ii = i + HALO;
+      const float* pl;
+      if (SLAB) {
+        pl = ii >= d.n1 ? hi + (int64_t)(ii - d.n1) * psz : fx + (int64_t)ii * psz;
+      } else {
+        ii = ii >= d.n1 ? ii - d.n1 : ii;
+        pl = fx + (int64_t)ii * psz;
+      }
+      w[8] = __ldg(pl + j * d.n3 + k);
     }
     float g1 = 0.f;
     if (active) {
@@ -83,7 +99,7 @@ __global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f
     const int64_t o = ((int64_t)i * d.n2 + j) * d.n3 + k;
     if (MODE == 0) {
       __syncthreads();
-      load_tile(tile, f, d, i + sx, j0, k0);
+      load_tile(tile, f, d, i, j0, k0);
       __syncthreads();
       if (active) {
         const int ty = threadIdx.y + HALO, tz = threadIdx.x + HALO;
@@ -100,7 +116,7 @@ __global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f
       }
     } else {
       __syncthreads();
-      load_tile(tile, f + cs, d, i + sx, j0, k0);
+      load_tile(tile, f + cs, d, i, j0, k0);
       __syncthreads();
       float acc = g1;
       if (active) {
@@ -111,7 +127,7 @@ __global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f
         acc = __fadd_rn(acc, fd8_combine(p, m, h2));
       }
       __syncthreads();
-      load_tile(tile, f + 2 * cs, d, i + sx, j0, k0);
+      load_tile(tile, f + 2 * cs, d, i, j0, k0);
       __syncthreads();
       if (active) {
         const int ty = threadIdx.y + HALO, tz = threadIdx.x + HALO;
@@ -131,50 +147,49 @@ __global__ void __launch_bounds__(TZ* TY) fd8_kernel(const float* __restrict__ f
 
 using namespace vr;
 
-// xoff < 0: periodic; xoff >= 4: slab with ghosts, n1_global gives the x1 spacing
-static int fd8_launch(int mode, const float* in, const int64_t dims[3], int xoff, int64_t n1_global, float* out,
-                      void* stream) {
+// lo/hi == nullptr: periodic; otherwise a slab with 4-plane ghost blocks
+static int fd8_launch(int mode, const float* in, const float* lo, const float* hi, const int64_t dims[3],
+                      int64_t n1_global, float* out, void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!in || !out || in == out) return VR_ERR_ARG;
-  const bool slab = xoff >= 0;
-  if (slab && xoff < HALO) return VR_ERR_ARG;
+  const bool slab = lo != nullptr;
+  if (slab && !hi) return VR_ERR_ARG;
   if ((!slab && d.n1 < 9) || d.n2 < 9 || d.n3 < 9 || n1_global < 9) return VR_ERR_DIMS;  // diffops.py:21,77-81
+  if (slab && d.n1 < HALO) return VR_ERR_DIMS;
   const float h1 = (float)(kTwoPi / n1_global), h2 = (float)(kTwoPi / d.n2), h3 = (float)(kTwoPi / d.n3);
   const int nx = 16;
   dim3 grid((d.n3 + TZ - 1) / TZ, (d.n2 + TY - 1) / TY, (d.n1 + nx - 1) / nx);
   dim3 block(TZ, TY);
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t cs = (int64_t)(d.n1 + 2 * (slab ? xoff : 0)) * d.n2 * d.n3;
   if (mode == 0 && slab)
-    fd8_kernel<0, true><<<grid, block, 0, s>>>(in, d, xoff, cs, h1, h2, h3, out, nx);
+    fd8_kernel<0, true><<<grid, block, 0, s>>>(in, lo, hi, d, h1, h2, h3, out, nx);
   else if (mode == 0)
-    fd8_kernel<0, false><<<grid, block, 0, s>>>(in, d, 0, cs, h1, h2, h3, out, nx);
+    fd8_kernel<0, false><<<grid, block, 0, s>>>(in, nullptr, nullptr, d, h1, h2, h3, out, nx);
   else if (slab)
-    fd8_kernel<1, true><<<grid, block, 0, s>>>(in, d, xoff, cs, h1, h2, h3, out, nx);
+    fd8_kernel<1, true><<<grid, block, 0, s>>>(in, lo, hi, d, h1, h2, h3, out, nx);
   else
-    fd8_kernel<1, false><<<grid, block, 0, s>>>(in, d, 0, cs, h1, h2, h3, out, nx);
+    fd8_kernel<1, false><<<grid, block, 0, s>>>(in, nullptr, nullptr, d, h1, h2, h3, out, nx);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
 extern "C" {
 int vr_fd8_grad(const float* f, const int64_t dims[3], float* out3, void* stream) {
-  return fd8_launch(0, f, dims, -1, dims ? dims[0] : 0, out3, stream);
+  return fd8_launch(0, f, nullptr, nullptr, dims, dims ? dims[0] : 0, out3, stream);
 }
 int vr_fd8_div(const float* v3, const int64_t dims[3], float* out, void* stream) {
-  return fd8_launch(1, v3, dims, -1, dims ? dims[0] : 0, out, stream);
+  return fd8_launch(1, v3, nullptr, nullptr, dims, dims ? dims[0] : 0, out, stream);
 }
-// x1-slab variants: dims = local (output) dims, input has xoff >= 4 ghost planes per side
-int vr_fd8_grad_slab(const float* f_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out3,
-                     void* stream) {
-  if (xoff < 0) return VR_ERR_ARG;
-  return fd8_launch(0, f_ext, dims, xoff, n1_global, out3, stream);
+int vr_fd8_grad_slab(const float* f, const float* f_lo, const float* f_hi, const int64_t dims[3], int64_t n1_global,
+                     float* out3, void* stream) {
+  if (!f_lo || !f_hi) return VR_ERR_ARG;
+  return fd8_launch(0, f, f_lo, f_hi, dims, n1_global, out3, stream);
 }
-int vr_fd8_div_slab(const float* v3_ext, const int64_t dims[3], int xoff, int64_t n1_global, float* out,
-                    void* stream) {
-  if (xoff < 0) return VR_ERR_ARG;
-  return fd8_launch(1, v3_ext, dims, xoff, n1_global, out, stream);
+int vr_fd8_div_slab(const float* v3, const float* v1_lo, const float* v1_hi, const int64_t dims[3],
+                    int64_t n1_global, float* out, void* stream) {
+  if (!v1_lo || !v1_hi) return VR_ERR_ARG;
+  return fd8_launch(1, v3, v1_lo, v1_hi, dims, n1_global, out, stream);
 }
 }

@@ -121,34 +121,52 @@ __device__ __forceinline__ void gather(const Src& src, const Dims& d, int ix, in
 
 // ---- lean gather for the transport sweeps --------------------------------------
 // Same arithmetic as gather<> but instruction-lean: the base index is wrapped
-// with one conditional per axis, every stencil row gets one row index and its
+// with one conditional per axis, every stencil row gets one row pointer and its
 // taps are immediate-offset loads unless the x3 window wraps at the end of the
-// row.  SLAB: the source is an x1 slab with `xoff` ghost planes on each side
-// (multi-GPU decomposition, dist.py): x1 is offset, never wrapped, and clamped
-// into the slab (the ghost width is sized from the global max displacement).
+// row.  SLAB: the source is this rank's x1 slab (L1 planes) plus separate
+// ghost blocks of w planes before (lo) and after (hi) it, filled by the host's
+// halo exchange (dist.py); x1 is never wrapped and is clamped into [-w, L1+w).
 __device__ __forceinline__ int wrap1(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 __device__ __forceinline__ int clampi(int i, int lo, int hi) { return i < lo ? lo : (i > hi ? hi : i); }
 
+// Component c of every block lives at base + c * stride (vector fields are
+// SoA: (3, L1, N2, N3) local, (3, w, N2, N3) ghosts).
+template <int NC, bool SLAB>
+struct PlaneSrc {
+  const float* mid;      // local field (periodic case: the whole field)
+  const float* lo;       // SLAB: ghost planes [-w, 0)
+  const float* hi;       // SLAB: ghost planes [L1, L1 + w)
+  int64_t mid_cs, ghost_cs;
+  int w, L1;
+  __device__ __forceinline__ const float* plane(int c, int x, int psz) const {
+    if (!SLAB) return mid + c * mid_cs + (int64_t)x * psz;
+    if (x < 0) return lo + c * ghost_cs + (int64_t)(x + w) * psz;
+    if (x < L1) return mid + c * mid_cs + (int64_t)x * psz;
+    return hi + c * ghost_cs + (int64_t)(x - L1) * psz;
+  }
+};
+
 template <int ORDER, int NC, bool SLAB>
-__device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, const Dims& ds, int ix, int iy,
-                                            int iz, float tx, float ty, float tz, float* out) {
-  // ds = SOURCE dims (for SLAB, ds.n1 includes the ghost planes and ix is already offset)
+__device__ __forceinline__ void gather_lean(const PlaneSrc<NC, SLAB>& src, const Dims& d, int ix, int iy, int iz,
+                                            float tx, float ty, float tz, float* out) {
+  // d = arrival dims (for SLAB d.n1 = L1); ix is a local x1 index
+  const int psz = d.n2 * d.n3;
   if (ORDER == ORDER_LINEAR) {
-    const int i0 = SLAB ? clampi(ix, 0, ds.n1 - 2) : wrap1(ix, ds.n1);
-    const int j0 = wrap1(iy, ds.n2), k0 = wrap1(iz, ds.n3);
-    const int i1 = SLAB ? i0 + 1 : next_wrap(i0, ds.n1), j1 = next_wrap(j0, ds.n2);
-    const bool zin = k0 + 1 < ds.n3;
-    const int dk = zin ? 1 : 1 - ds.n3;
-    const int r00 = (i0 * ds.n2 + j0) * ds.n3 + k0, r01 = (i0 * ds.n2 + j1) * ds.n3 + k0;
-    const int r10 = (i1 * ds.n2 + j0) * ds.n3 + k0, r11 = (i1 * ds.n2 + j1) * ds.n3 + k0;
+    const int i0 = SLAB ? clampi(ix, -src.w, src.L1 + src.w - 2) : wrap1(ix, d.n1);
+    const int j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
+    const int i1 = SLAB ? i0 + 1 : next_wrap(i0, d.n1), j1 = next_wrap(j0, d.n2);
+    const bool zin = k0 + 1 < d.n3;
+    const int dk = zin ? 1 : 1 - d.n3;
+    const int r0 = j0 * d.n3 + k0, r1 = j1 * d.n3 + k0;
     const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      const float* b = p[c];
-      const float c00 = __ldg(b + r00) * sz + __ldg(b + r00 + dk) * tz;
-      const float c01 = __ldg(b + r01) * sz + __ldg(b + r01 + dk) * tz;
-      const float c10 = __ldg(b + r10) * sz + __ldg(b + r10 + dk) * tz;
-      const float c11 = __ldg(b + r11) * sz + __ldg(b + r11 + dk) * tz;
+      const float* b0 = src.plane(c, i0, psz);
+      const float* b1 = src.plane(c, i1, psz);
+      const float c00 = __ldg(b0 + r0) * sz + __ldg(b0 + r0 + dk) * tz;
+      const float c01 = __ldg(b0 + r1) * sz + __ldg(b0 + r1 + dk) * tz;
+      const float c10 = __ldg(b1 + r0) * sz + __ldg(b1 + r0 + dk) * tz;
+      const float c11 = __ldg(b1 + r1) * sz + __ldg(b1 + r1 + dk) * tz;
       const float c0 = c00 * sy + c01 * ty;
       const float c1 = c10 * sy + c11 * ty;
       out[c] = c0 * sx + c1 * tx;
@@ -158,19 +176,19 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
     lagrange4(tx, wx);
     lagrange4(ty, wy);
     lagrange4(tz, wz);
-    const int j0 = wrap1(iy, ds.n2), k0 = wrap1(iz, ds.n3);
+    const int j0 = wrap1(iy, d.n2), k0 = wrap1(iz, d.n3);
     int xo[4], yo[4];
     if (SLAB) {
-      const int i0 = clampi(ix, 1, ds.n1 - 3);
+      const int i0 = clampi(ix, 1 - src.w, src.L1 + src.w - 3);
       xo[0] = i0 - 1; xo[1] = i0; xo[2] = i0 + 1; xo[3] = i0 + 2;
     } else {
-      cubic_idx(wrap1(ix, ds.n1), ds.n1, xo);
+      cubic_idx(wrap1(ix, d.n1), d.n1, xo);
     }
-    cubic_idx(j0, ds.n2, yo);
+    cubic_idx(j0, d.n2, yo);
     float acc[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = 0.0f;
-    if (k0 >= 1 && k0 + 2 < ds.n3) {  // x3 window inside the row: immediate-offset taps
+    if (k0 >= 1 && k0 + 2 < d.n3) {  // x3 window inside the row: immediate-offset taps
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         float sa[NC];
@@ -178,10 +196,9 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
         for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int row = (xo[a] * ds.n2 + yo[b]) * ds.n3 + (k0 - 1);   // < 2^31 (dims_from)
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            const float* r = p[c] + row;
+            const float* r = src.plane(c, xo[a], psz) + (yo[b] * d.n3 + k0 - 1);
             const float sb = wz[0] * __ldg(r) + wz[1] * __ldg(r + 1) + wz[2] * __ldg(r + 2) + wz[3] * __ldg(r + 3);
             sa[c] += wy[b] * sb;
           }
@@ -191,7 +208,7 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
       }
     } else {
       int zo[4];
-      cubic_idx(k0, ds.n3, zo);
+      cubic_idx(k0, d.n3, zo);
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         float sa[NC];
@@ -199,12 +216,11 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
         for (int c = 0; c < NC; ++c) sa[c] = 0.0f;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int row = (xo[a] * ds.n2 + yo[b]) * ds.n3;
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            const float* r = p[c] + row;
-            const float sb = wz[0] * __ldg(r + zo[0]) + wz[1] * __ldg(r + zo[1]) + wz[2] * __ldg(r + zo[2]) +
-                             wz[3] * __ldg(r + zo[3]);
+            const float* row = src.plane(c, xo[a], psz) + yo[b] * d.n3;
+            const float sb = wz[0] * __ldg(row + zo[0]) + wz[1] * __ldg(row + zo[1]) + wz[2] * __ldg(row + zo[2]) +
+                             wz[3] * __ldg(row + zo[3]);
             sa[c] += wy[b] * sb;
           }
         }
@@ -217,27 +233,20 @@ __device__ __forceinline__ void gather_lean(const float* const* __restrict__ p, 
   }
 }
 
-// Departure point of arrival voxel (i,j,k) (local index) displaced by -(d1,d2,d3).
-// d = ARRIVAL dims; the source has d.n1 + 2*xoff x1 planes when SLAB.  Huge
+// Departure point of arrival voxel (i,j,k) displaced by -(d1,d2,d3); huge
 // displacements (|d| >= n - 4) are pre-wrapped with a full modulo.
 template <int ORDER, int NC, bool SLAB>
-__device__ __forceinline__ void gather_disp_lean(const float* const* p, const Dims& d, int xoff, int i, int j, int k,
+__device__ __forceinline__ void gather_disp_lean(const PlaneSrc<NC, SLAB>& src, const Dims& d, int i, int j, int k,
                                                  float d1, float d2, float d3, float* out) {
   int ix, iy, iz;
   float tx, ty, tz;
   split_coord(i, d1, ix, tx);
   split_coord(j, d2, iy, ty);
   split_coord(k, d3, iz, tz);
-  Dims ds = d;
-  if (SLAB) {
-    ds.n1 = d.n1 + 2 * xoff;
-    ix += xoff;
-  } else if (!(fabsf(d1) < d.n1 - 4)) {
-    ix = wrap_idx(ix, d.n1);
-  }
+  if (!SLAB && !(fabsf(d1) < d.n1 - 4)) ix = wrap_idx(ix, d.n1);
   if (!(fabsf(d2) < d.n2 - 4)) iy = wrap_idx(iy, d.n2);
   if (!(fabsf(d3) < d.n3 - 4)) iz = wrap_idx(iz, d.n3);
-  gather_lean<ORDER, NC, SLAB>(p, ds, ix, iy, iz, tx, ty, tz, out);
+  gather_lean<ORDER, NC, SLAB>(src, d, ix, iy, iz, tx, ty, tz, out);
 }
 
 // Gather at voxel (i,j,k) displaced by -(d1,d2,d3) index units.

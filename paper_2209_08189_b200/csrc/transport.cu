@@ -64,32 +64,52 @@ __global__ void __launch_bounds__(256) interp_points_kernel(const float* __restr
 //   x* = x - dt v(x);  X = x - dt/2 (v(x) + v(x*))           (forward)
 //   backward trace is the same with -v (transport.py:102)
 //   jac = (1 + dt/2 div(X_f)) / (1 - dt/2 div(x)),  adj likewise with X_b
-// SLAB: v / div are x1 slabs with `xoff` ghost planes per side (component
-// stride Ne); outputs are the local slab.
+// Uses the general flat-index gather (its 3-component form keeps register
+// pressure low; the trace runs once per velocity iterate).  SLAB: v and div are
+// contiguous ghost-extended slabs of L1 + 2w planes (component stride Ne); the
+// departure x1 index is shifted by w and clamped instead of wrapped.
+template <int ORDER, bool SLAB>
+__device__ __forceinline__ void trace_gather(const float* const* p, const Dims& ds, int w, int i, int j, int k,
+                                             float d1, float d2, float d3, float* out, int nc) {
+  int ix, iy, iz;
+  float tx, ty, tz;
+  split_coord(i, d1, ix, tx);
+  split_coord(j, d2, iy, ty);
+  split_coord(k, d3, iz, tz);
+  if (SLAB) ix = clampi(ix + w, 1, ds.n1 - 3);
+  SrcF32 s{{p[0], p[nc > 1 ? 1 : 0], p[nc > 2 ? 2 : 0]}, 0};
+  if (nc == 3)
+    gather<ORDER, 3>(s, ds, ix, iy, iz, tx, ty, tz, out);
+  else
+    gather<ORDER, 1>(s, ds, ix, iy, iz, tx, ty, tz, out);
+}
+
 template <int ORDER, bool FACTORS, bool SLAB>
-__global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v, Dims d, int xoff, int64_t Ne,
-                                                    float dt, float ih1, float ih2, float ih3,
-                                                    float* __restrict__ disp_f, float* __restrict__ disp_b,
-                                                    const float* __restrict__ div,
+__global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v, Dims d, int w, float dt, float ih1,
+                                                    float ih2, float ih3, float* __restrict__ disp_f,
+                                                    float* __restrict__ disp_b, const float* __restrict__ div,
                                                     float* __restrict__ fac_f, float* __restrict__ fac_b) {
   const int64_t N = d.n();
-  const Vox p = vox3(d);
-  if (!p.ok) return;
-  const int i = p.i, j = p.j, k = p.k, idx = p.idx;
-  const int sidx = SLAB ? idx + xoff * d.n2 * d.n3 : idx;   // own voxel in the source slab
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  const Dims ds{SLAB ? d.n1 + 2 * w : d.n1, d.n2, d.n3};   // source dims
+  const int64_t Ne = ds.n();
+  const int sidx = SLAB ? idx + w * d.n2 * d.n3 : idx;    // own voxel in the source
   const float v1 = __ldg(v + sidx), v2 = __ldg(v + Ne + sidx), v3 = __ldg(v + 2 * Ne + sidx);
   const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
   const float* sv[3] = {v, v + Ne, v + 2 * Ne};
   float vs[3];
   const float half = 0.5f * dt;
   // forward: x* = x - dt v
-  gather_disp_lean<ORDER, 3, SLAB>(sv, d, xoff, i, j, k, a1, a2, a3, vs);
+  trace_gather<ORDER, SLAB>(sv, ds, w, i, j, k, a1, a2, a3, vs, 3);
   const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
   disp_f[idx] = f1;
   disp_f[N + idx] = f2;
   disp_f[2 * N + idx] = f3;
   // backward: x* = x + dt v, X = x + dt/2 (v + v(x*))
-  gather_disp_lean<ORDER, 3, SLAB>(sv, d, xoff, i, j, k, -a1, -a2, -a3, vs);
+  trace_gather<ORDER, SLAB>(sv, ds, w, i, j, k, -a1, -a2, -a3, vs, 3);
   const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
   disp_b[idx] = b1;
   disp_b[N + idx] = b2;
@@ -98,9 +118,9 @@ __global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v,
     const float* sd[1] = {div};
     const float denom = 1.0f - half * __ldg(div + sidx);
     float dv;
-    gather_disp_lean<ORDER, 1, SLAB>(sd, d, xoff, i, j, k, f1, f2, f3, &dv);
+    trace_gather<ORDER, SLAB>(sd, ds, w, i, j, k, f1, f2, f3, &dv, 1);
     fac_f[idx] = (1.0f + half * dv) / denom;
-    gather_disp_lean<ORDER, 1, SLAB>(sd, d, xoff, i, j, k, b1, b2, b3, &dv);
+    trace_gather<ORDER, SLAB>(sd, ds, w, i, j, k, b1, b2, b3, &dv, 1);
     fac_b[idx] = (1.0f + half * dv) / denom;
   }
 }
@@ -110,17 +130,15 @@ __global__ void __launch_bounds__(128) trace_kernel(const float* __restrict__ v,
 // adjoint: transport.py:154-155 (factor = adj_numer/adj_denom, backward trace)
 // jacobian: transport.py:194-195 (factor = jac_numer/jac_denom)
 template <int ORDER, bool SCALE, bool SLAB>
-__global__ void __launch_bounds__(128) advect_kernel(const float* __restrict__ src, Dims d, int xoff,
-                                                     const float* __restrict__ disp,
+__global__ void __launch_bounds__(128) advect_kernel(PlaneSrc<1, SLAB> src, Dims d, const float* __restrict__ disp,
                                                      const float* __restrict__ fac, float* __restrict__ dst,
                                                      int* flag) {
   const int64_t N = d.n();
   const Vox p = vox3(d);
   if (!p.ok) return;
   const int idx = p.idx;
-  const float* sp[1] = {src};
   float o;
-  gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+  gather_disp_lean<ORDER, 1, SLAB>(src, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
                                    __ldg(disp + 2 * N + idx), &o);
   if (SCALE) o *= __ldg(fac + idx);
   dst[idx] = o;
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(256) incstate_init_kernel(const float* __restr
 }
 
 template <int ORDER, bool SLAB>
-__global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restrict__ u, Dims d, int xoff,
+__global__ void __launch_bounds__(128) incstate_step_kernel(PlaneSrc<1, SLAB> u, Dims d,
                                                             const float* __restrict__ disp,
                                                             const float* __restrict__ vt,
                                                             const float* __restrict__ gnext, float half,
@@ -154,9 +172,8 @@ __global__ void __launch_bounds__(128) incstate_step_kernel(const float* __restr
   const Vox p = vox3(d);
   if (!p.ok) return;
   const int idx = p.idx;
-  const float* sp[1] = {u};
   float o;
-  gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
+  gather_disp_lean<ORDER, 1, SLAB>(u, d, p.i, p.j, p.k, __ldg(disp + idx), __ldg(disp + N + idx),
                                    __ldg(disp + 2 * N + idx), &o);
   const float hs = half * inc_source(vt, gnext, N, idx);
   float m = o + hs;
@@ -192,9 +209,8 @@ __global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict
 // step thresholds at 0.5 and writes `id` (labels processed in ascending order, so
 // overlaps resolve to the larger id as in the reference).
 template <int ORDER, bool FROM_LABELS, bool TO_LABELS, bool SLAB>
-__global__ void __launch_bounds__(128) label_step_kernel(const float* __restrict__ src,
-                                                         const int* __restrict__ lab_in, int id, Dims d, int xoff,
-                                                         const float* __restrict__ disp,
+__global__ void __launch_bounds__(128) label_step_kernel(PlaneSrc<1, SLAB> src, const int* __restrict__ lab_in,
+                                                         int id, Dims d, const float* __restrict__ disp,
                                                          float* __restrict__ dst, int* __restrict__ lab_out) {
   const int64_t N = d.n();
   const Vox p = vox3(d);
@@ -206,14 +222,24 @@ __global__ void __launch_bounds__(128) label_step_kernel(const float* __restrict
     SrcLabel s{lab_in, id};
     gather_disp<ORDER, 1>(s, d, i, j, k, d1, d2, d3, &o);
   } else {
-    const float* sp[1] = {src};
-    gather_disp_lean<ORDER, 1, SLAB>(sp, d, xoff, i, j, k, d1, d2, d3, &o);
+    gather_disp_lean<ORDER, 1, SLAB>(src, d, i, j, k, d1, d2, d3, &o);
   }
   if (TO_LABELS) {
     if (o >= 0.5f) lab_out[idx] = id;
   } else {
     dst[idx] = o;
   }
+}
+
+template <int NC>
+PlaneSrc<NC, true> slab_src(const float* mid, const float* lo, const float* hi, int64_t mid_cs, int64_t ghost_cs,
+                            int w, int L1) {
+  return PlaneSrc<NC, true>{mid, lo, hi, mid_cs, ghost_cs, w, L1};
+}
+
+template <int NC>
+PlaneSrc<NC, false> full_src(const float* mid, int64_t cs) {
+  return PlaneSrc<NC, false>{mid, mid, mid, cs, cs, 0, 0};
 }
 
 // ---- displacement -> absolute points in radians (Characteristics.points) ----
@@ -274,85 +300,93 @@ int vr_interp_points(const float* src, const int64_t dims[3], const void* pts, i
 
 }  // extern "C"
 
-// xoff < 0: periodic single-domain call; xoff >= 0: x1 slab with xoff ghost planes
-static int trace_impl(const float* v, const int64_t dims[3], int xoff, double dt, int order, float* disp_fwd,
-                      float* disp_bwd, const float* div, float* fac_jac, float* fac_adj, void* stream) {
+// Slab arguments: lo/hi == nullptr -> periodic single-domain call; otherwise the
+// source is the local slab (L1 = dims[0] planes) with w ghost planes in lo / hi.
+struct SlabArgs {
+  const float* lo;
+  const float* hi;
+  int w;
+  bool on() const { return lo != nullptr; }
+};
+
+static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, int w, const float* div, double dt,
+                      int order, float* disp_fwd, float* disp_bwd, float* fac_jac, float* fac_adj, void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!v || !disp_fwd || !disp_bwd || !(dt > 0)) return VR_ERR_ARG;
   const bool factors = div != nullptr;
   if (factors && (!fac_jac || !fac_adj)) return VR_ERR_ARG;
+  const bool slab = w >= 0;
+  if (slab && (w < 2 || w > d.n1)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  // spacing of the GLOBAL lattice: for a slab call dims[0] is the local plane
-  // count, the x1 spacing is passed through dims[3] (global N1) by the slab entry
-  const float ih1 = (float)(d.n1 / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
-  const dim3 g = vox_grid(d);
-  const int tpb = vox_tpb(d);
-  const int64_t Ne = (int64_t)(d.n1 + 2 * (xoff > 0 ? xoff : 0)) * d.n2 * d.n3;
+  const float ih1 = (float)(n1_global / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
+  const unsigned g = grid_for(d.n(), 256);
   VR_DISPATCH_ORDER(order, {
-    if (xoff >= 0) {
-      const float gih1 = (float)(dims[3] / kTwoPi);
-      if (factors)
-        trace_kernel<ORD, true, true><<<g, tpb, 0, s>>>(v, d, xoff, Ne, (float)dt, gih1, ih2, ih3, disp_fwd,
-                                                        disp_bwd, div, fac_jac, fac_adj);
-      else
-        trace_kernel<ORD, false, true><<<g, tpb, 0, s>>>(v, d, xoff, Ne, (float)dt, gih1, ih2, ih3, disp_fwd,
-                                                         disp_bwd, nullptr, nullptr, nullptr);
-    } else if (factors) {
-      trace_kernel<ORD, true, false><<<g, tpb, 0, s>>>(v, d, 0, Ne, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
-                                                       div, fac_jac, fac_adj);
-    } else {
-      trace_kernel<ORD, false, false><<<g, tpb, 0, s>>>(v, d, 0, Ne, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+    if (slab && factors)
+      trace_kernel<ORD, true, true><<<g, 256, 0, s>>>(v, d, w, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
+                                                      fac_jac, fac_adj);
+    else if (slab)
+      trace_kernel<ORD, false, true><<<g, 256, 0, s>>>(v, d, w, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                       nullptr, nullptr, nullptr);
+    else if (factors)
+      trace_kernel<ORD, true, false><<<g, 256, 0, s>>>(v, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
+                                                       fac_jac, fac_adj);
+    else
+      trace_kernel<ORD, false, false><<<g, 256, 0, s>>>(v, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
                                                         nullptr, nullptr, nullptr);
-    }
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
-static int advect_impl(const float* src, const int64_t dims[3], int xoff, const float* disp, const float* factor,
+static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], const float* disp, const float* factor,
                        int order, float* dst, int* nonfinite_flag, void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!src || !disp || !dst || src == dst) return VR_ERR_ARG;
+  if (sg.on() && (sg.w < 1 || sg.w > d.n1 || !sg.hi)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
-    if (xoff >= 0) {
+    if (sg.on()) {
+      auto ps = slab_src<1>(src, sg.lo, sg.hi, 0, 0, sg.w, d.n1);
       if (factor)
-        advect_kernel<ORD, true, true><<<g, tpb, 0, s>>>(src, d, xoff, disp, factor, dst, nonfinite_flag);
+        advect_kernel<ORD, true, true><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag);
       else
-        advect_kernel<ORD, false, true><<<g, tpb, 0, s>>>(src, d, xoff, disp, nullptr, dst, nonfinite_flag);
-    } else if (factor) {
-      advect_kernel<ORD, true, false><<<g, tpb, 0, s>>>(src, d, 0, disp, factor, dst, nonfinite_flag);
+        advect_kernel<ORD, false, true><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag);
     } else {
-      advect_kernel<ORD, false, false><<<g, tpb, 0, s>>>(src, d, 0, disp, nullptr, dst, nonfinite_flag);
+      auto ps = full_src<1>(src, 0);
+      if (factor)
+        advect_kernel<ORD, true, false><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag);
+      else
+        advect_kernel<ORD, false, false><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag);
     }
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
-static int incstate_impl(const float* u, const int64_t dims[3], int xoff, const float* disp_fwd, const float* vt,
+static int incstate_impl(const float* u, SlabArgs sg, const int64_t dims[3], const float* disp_fwd, const float* vt,
                          const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
                          void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
+  if (sg.on() && (sg.w < 1 || sg.w > d.n1 || !sg.hi)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
-    if (xoff >= 0)
-      incstate_step_kernel<ORD, true><<<g, tpb, 0, s>>>(u, d, xoff, disp_fwd, vt, gradm_next, (float)(0.5 * dt),
-                                                        last, out, nonfinite_flag);
+    if (sg.on())
+      incstate_step_kernel<ORD, true><<<g, tpb, 0, s>>>(slab_src<1>(u, sg.lo, sg.hi, 0, 0, sg.w, d.n1), d, disp_fwd,
+                                                        vt, gradm_next, (float)(0.5 * dt), last, out, nonfinite_flag);
     else
-      incstate_step_kernel<ORD, false><<<g, tpb, 0, s>>>(u, d, 0, disp_fwd, vt, gradm_next, (float)(0.5 * dt),
-                                                         last, out, nonfinite_flag);
+      incstate_step_kernel<ORD, false><<<g, tpb, 0, s>>>(full_src<1>(u, 0), d, disp_fwd, vt, gradm_next,
+                                                         (float)(0.5 * dt), last, out, nonfinite_flag);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -362,26 +396,27 @@ extern "C" {
 
 int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, float* disp_fwd, float* disp_bwd,
                  const float* div, float* fac_jac, float* fac_adj, void* stream) {
-  return trace_impl(v, dims, -1, dt, order, disp_fwd, disp_bwd, div, fac_jac, fac_adj, stream);
+  if (!dims) return VR_ERR_ARG;
+  return trace_impl(v, dims, dims[0], -1, div, dt, order, disp_fwd, disp_bwd, fac_jac, fac_adj, stream);
 }
 
-// x1-slab variant: dims4 = {L1 (local planes), N2, N3, N1 (global planes)};
-// v (3 comps) and div carry `xoff` ghost planes on each side.
-int vr_trace_rk2_slab(const float* v_ext, const int64_t dims4[4], int xoff, double dt, int order, float* disp_fwd,
-                      float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj, void* stream) {
-  if (xoff < 0) return VR_ERR_ARG;
-  return trace_impl(v_ext, dims4, xoff, dt, order, disp_fwd, disp_bwd, div_ext, fac_jac, fac_adj, stream);
+int vr_trace_rk2_slab(const float* v_ext, const int64_t dims[3], int64_t n1_global, int w, double dt, int order,
+                      float* disp_fwd, float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj,
+                      void* stream) {
+  if (w < 0) return VR_ERR_ARG;
+  return trace_impl(v_ext, dims, n1_global, w, div_ext, dt, order, disp_fwd, disp_bwd, fac_jac, fac_adj, stream);
 }
 
 int vr_advect(const float* src, const int64_t dims[3], const float* disp, const float* factor, int order,
               float* dst, int* nonfinite_flag, void* stream) {
-  return advect_impl(src, dims, -1, disp, factor, order, dst, nonfinite_flag, stream);
+  return advect_impl(src, SlabArgs{nullptr, nullptr, 0}, dims, disp, factor, order, dst, nonfinite_flag, stream);
 }
 
-int vr_advect_slab(const float* src_ext, const int64_t dims[3], int xoff, const float* disp, const float* factor,
-                   int order, float* dst, int* nonfinite_flag, void* stream) {
-  if (xoff < 0) return VR_ERR_ARG;
-  return advect_impl(src_ext, dims, xoff, disp, factor, order, dst, nonfinite_flag, stream);
+int vr_advect_slab(const float* src, const float* src_lo, const float* src_hi, const int64_t dims[3], int w,
+                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag,
+                   void* stream) {
+  if (!src_lo || !src_hi) return VR_ERR_ARG;
+  return advect_impl(src, SlabArgs{src_lo, src_hi, w}, dims, disp, factor, order, dst, nonfinite_flag, stream);
 }
 
 int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3], double dt, float* u0,
@@ -399,14 +434,16 @@ int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3]
 int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fwd, const float* vt,
                      const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
                      void* stream) {
-  return incstate_impl(u, dims, -1, disp_fwd, vt, gradm_next, dt, order, last, out, nonfinite_flag, stream);
+  return incstate_impl(u, SlabArgs{nullptr, nullptr, 0}, dims, disp_fwd, vt, gradm_next, dt, order, last, out,
+                       nonfinite_flag, stream);
 }
 
-int vr_incstate_step_slab(const float* u_ext, const int64_t dims[3], int xoff, const float* disp_fwd,
-                          const float* vt, const float* gradm_next, double dt, int order, int last, float* out,
-                          int* nonfinite_flag, void* stream) {
-  if (xoff < 0) return VR_ERR_ARG;
-  return incstate_impl(u_ext, dims, xoff, disp_fwd, vt, gradm_next, dt, order, last, out, nonfinite_flag, stream);
+int vr_incstate_step_slab(const float* u, const float* u_lo, const float* u_hi, const int64_t dims[3], int w,
+                          const float* disp_fwd, const float* vt, const float* gradm_next, double dt, int order,
+                          int last, float* out, int* nonfinite_flag, void* stream) {
+  if (!u_lo || !u_hi) return VR_ERR_ARG;
+  return incstate_impl(u, SlabArgs{u_lo, u_hi, w}, dims, disp_fwd, vt, gradm_next, dt, order, last, out,
+                       nonfinite_flag, stream);
 }
 
 int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
@@ -431,41 +468,41 @@ int vr_label_step(const float* src, const int* labels_in, int label_id, const in
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
   const bool from_l = labels_in != nullptr, to_l = labels_out != nullptr;
+  auto ps = full_src<1>(src ? src : reinterpret_cast<const float*>(labels_in), 0);
   VR_DISPATCH_ORDER(order, {
     if (from_l && to_l)
-      label_step_kernel<ORD, true, true, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, 0, disp, nullptr,
+      label_step_kernel<ORD, true, true, false><<<g, tpb, 0, s>>>(ps, labels_in, label_id, d, disp, nullptr,
                                                                   labels_out);
     else if (from_l)
-      label_step_kernel<ORD, true, false, false><<<g, tpb, 0, s>>>(nullptr, labels_in, label_id, d, 0, disp, dst,
-                                                                   nullptr);
+      label_step_kernel<ORD, true, false, false><<<g, tpb, 0, s>>>(ps, labels_in, label_id, d, disp, dst, nullptr);
     else if (to_l)
-      label_step_kernel<ORD, false, true, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, 0, disp, nullptr,
+      label_step_kernel<ORD, false, true, false><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, nullptr,
                                                                    labels_out);
     else
-      label_step_kernel<ORD, false, false, false><<<g, tpb, 0, s>>>(src, nullptr, label_id, d, 0, disp, dst,
-                                                                    nullptr);
+      label_step_kernel<ORD, false, false, false><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
-// slab label step from a float indicator / advected field with ghost planes
-int vr_label_step_slab(const float* src_ext, int label_id, const int64_t dims[3], int xoff, const float* disp,
-                       int order, float* dst, int* labels_out, void* stream) {
+// slab label step from a float indicator / advected field with ghost blocks
+int vr_label_step_slab(const float* src, const float* src_lo, const float* src_hi, int label_id,
+                       const int64_t dims[3], int w, const float* disp, int order, float* dst, int* labels_out,
+                       void* stream) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
-  if (!src_ext || !disp || xoff < 0 || (!dst && !labels_out)) return VR_ERR_ARG;
+  if (!src || !src_lo || !src_hi || !disp || w < 1 || w > d.n1 || (!dst && !labels_out)) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g = vox_grid(d);
   const int tpb = vox_tpb(d);
+  auto ps = slab_src<1>(src, src_lo, src_hi, 0, 0, w, d.n1);
   VR_DISPATCH_ORDER(order, {
     if (labels_out)
-      label_step_kernel<ORD, false, true, true><<<g, tpb, 0, s>>>(src_ext, nullptr, label_id, d, xoff, disp,
-                                                                  nullptr, labels_out);
+      label_step_kernel<ORD, false, true, true><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, nullptr,
+                                                                  labels_out);
     else
-      label_step_kernel<ORD, false, false, true><<<g, tpb, 0, s>>>(src_ext, nullptr, label_id, d, xoff, disp, dst,
-                                                                   nullptr);
+      label_step_kernel<ORD, false, false, true><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;

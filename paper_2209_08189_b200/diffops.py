@@ -208,9 +208,9 @@ def fd8_gradient_t(f: torch.Tensor, out: torch.Tensor | None = None) -> torch.Te
         out = torch.empty((3,) + dims, dtype=torch.float32, device=f.device)
     ctx = dist.current()
     if ctx is not None:   # x1 slab: 4 ghost planes from the neighbours
-        ext = ctx.halo(f, 4)
-        _lib.check(_lib.lib().vr_fd8_grad_slab(ext.data_ptr(), _lib.dims_arg(dims), 4, ctx.dims[0],
-                                               out.data_ptr(), _lib.stream()), "vr_fd8_grad_slab")
+        lo, hi = ctx.ghosts(f, 4)
+        _lib.check(_lib.lib().vr_fd8_grad_slab(f.data_ptr(), lo.data_ptr(), hi.data_ptr(), _lib.dims_arg(dims),
+                                               ctx.dims[0], out.data_ptr(), _lib.stream()), "vr_fd8_grad_slab")
         return out
     _lib.check(_lib.lib().vr_fd8_grad(f.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
                "vr_fd8_grad")
@@ -223,10 +223,10 @@ def fd8_divergence_t(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.
     if out is None:
         out = torch.empty(dims, dtype=torch.float32, device=v.device)
     ctx = dist.current()
-    if ctx is not None:
-        ext = ctx.halo(v, 4)
-        _lib.check(_lib.lib().vr_fd8_div_slab(ext.data_ptr(), _lib.dims_arg(dims), 4, ctx.dims[0], out.data_ptr(),
-                                              _lib.stream()), "vr_fd8_div_slab")
+    if ctx is not None:   # only v1 is differentiated along x1
+        lo, hi = ctx.ghosts(v[0], 4)
+        _lib.check(_lib.lib().vr_fd8_div_slab(v.data_ptr(), lo.data_ptr(), hi.data_ptr(), _lib.dims_arg(dims),
+                                              ctx.dims[0], out.data_ptr(), _lib.stream()), "vr_fd8_div_slab")
         return out
     _lib.check(_lib.lib().vr_fd8_div(v.data_ptr(), _lib.dims_arg(dims), out.data_ptr(), _lib.stream()),
                "vr_fd8_div")

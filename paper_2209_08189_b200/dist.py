@@ -27,6 +27,8 @@ import numpy as np
 import torch
 import torch.distributed as tdist
 
+from . import _lib
+
 _CTX = None
 
 
@@ -74,35 +76,45 @@ class SlabContext:
         tdist.all_reduce(t, op=rop, group=self.group)
         return t.cpu().numpy()
 
+    def allreduce_(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:
+        """In-place allreduce of a device tensor (no host round trip)."""
+        rop = {"sum": tdist.ReduceOp.SUM, "max": tdist.ReduceOp.MAX, "min": tdist.ReduceOp.MIN}[op]
+        with _lib.timed("dist.allreduce"):
+            tdist.all_reduce(t, op=rop, group=self.group)
+        return t
+
     # ---- ghost planes --------------------------------------------------------------
-    def halo(self, x: torch.Tensor, w: int, out: torch.Tensor | None = None) -> torch.Tensor:
-        """(..., L1, N2, N3) local slab -> (..., L1 + 2w, N2, N3) with w periodic
-        ghost planes on each side taken from the x1 neighbours."""
+    def ghosts(self, x: torch.Tensor, w: int) -> tuple:
+        """(lo, hi) ghost blocks (..., w, N2, N3) of the local slab x (..., L1, N2, N3):
+        lo = the w periodic planes preceding this slab, hi = the w following it.
+        The slab itself is not copied; kernels read lo / x / hi by plane."""
         L1 = x.shape[-3]
         if w > L1:
             raise ValueError(f"ghost width {w} exceeds the slab depth {L1}; use fewer ranks")
-        shape = tuple(x.shape[:-3]) + (L1 + 2 * w,) + tuple(x.shape[-2:])
-        ext = out if out is not None else torch.empty(shape, dtype=x.dtype, device=x.device)
-        ext[..., w:w + L1, :, :].copy_(x)
-        if w == 0:
-            return ext
+        send_lo = x[..., :w, :, :]            # -> left neighbour's hi ghost
+        send_hi = x[..., L1 - w:, :, :]       # -> right neighbour's lo ghost
         if self.world == 1:
-            ext[..., :w, :, :].copy_(x[..., L1 - w:, :, :])
-            ext[..., w + L1:, :, :].copy_(x[..., :w, :, :])
-            return ext
-        send_lo = x[..., :w, :, :].contiguous()          # -> left neighbour's right ghost
-        send_hi = x[..., L1 - w:, :, :].contiguous()     # -> right neighbour's left ghost
-        recv_hi = torch.empty_like(send_lo)              # <- right neighbour's first planes
-        recv_lo = torch.empty_like(send_hi)              # <- left neighbour's last planes
+            return send_hi.contiguous(), send_lo.contiguous()
+        with _lib.timed("dist.ghosts"):
+            return self._exchange_ghosts(send_lo, send_hi)
+
+    def _exchange_ghosts(self, send_lo, send_hi):
+        send_lo = send_lo.contiguous()
+        send_hi = send_hi.contiguous()
+        hi = torch.empty_like(send_lo)        # <- right neighbour's first planes
+        lo = torch.empty_like(send_hi)        # <- left neighbour's last planes
         ops = [tdist.P2POp(tdist.isend, send_lo, self.left, self.group),
                tdist.P2POp(tdist.isend, send_hi, self.right, self.group),
-               tdist.P2POp(tdist.irecv, recv_hi, self.right, self.group),
-               tdist.P2POp(tdist.irecv, recv_lo, self.left, self.group)]
+               tdist.P2POp(tdist.irecv, hi, self.right, self.group),
+               tdist.P2POp(tdist.irecv, lo, self.left, self.group)]
         for req in tdist.batch_isend_irecv(ops):
             req.wait()
-        ext[..., :w, :, :].copy_(recv_lo)
-        ext[..., w + L1:, :, :].copy_(recv_hi)
-        return ext
+        return lo, hi
+
+    def halo(self, x: torch.Tensor, w: int) -> torch.Tensor:
+        """(..., L1, N2, N3) -> (..., L1 + 2w, N2, N3) extended copy (tests / tools)."""
+        lo, hi = self.ghosts(x, w)
+        return torch.cat([lo, x, hi], dim=-3)
 
     # ---- transposes -------------------------------------------------------------
     def alltoall(self, out: torch.Tensor, inp: torch.Tensor) -> None:
@@ -110,7 +122,8 @@ class SlabContext:
         if self.world == 1:
             out.copy_(inp)
             return
-        tdist.all_to_all_single(out, inp, group=self.group)
+        with _lib.timed("dist.alltoall"):
+            tdist.all_to_all_single(out, inp, group=self.group)
 
     # ---- synthetic-input helpers -------------------------------------------------
     def local_coords(self) -> np.ndarray:

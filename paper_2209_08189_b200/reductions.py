@@ -15,10 +15,13 @@ def _n(t: torch.Tensor) -> int:
     return t.numel()
 
 
-def _sum(x: np.ndarray) -> np.ndarray:
-    """Cross-rank sum of partial results when a slab decomposition is active."""
+def _sum(out: torch.Tensor) -> np.ndarray:
+    """Host copy of a device result vector, summed across ranks (on device) when
+    a slab decomposition is active."""
     ctx = _dist.current()
-    return x if ctx is None else ctx.allreduce(x, "sum")
+    if ctx is not None:
+        ctx.allreduce_(out, "sum")
+    return out.cpu().numpy()
 
 
 def dots(pairs) -> np.ndarray:
@@ -31,7 +34,7 @@ def dots(pairs) -> np.ndarray:
     a = _lib.ptr_array([p[0] for p in pairs])
     b = _lib.ptr_array([p[1] for p in pairs])
     _lib.check(lib.vr_dots(k, a, b, n, _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()), "vr_dots")
-    return _sum(out.cpu().numpy())
+    return _sum(out)
 
 
 def dot(a: torch.Tensor, b: torch.Tensor) -> float:
@@ -43,7 +46,7 @@ def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> n
     out = _lib.out_buf(2)
     _lib.check(lib.vr_sqdiff(a.data_ptr(), b.data_ptr(), _lib.ptr(c), _n(a), _lib.scratch().data_ptr(),
                              out.data_ptr(), _lib.stream()), "vr_sqdiff")
-    return _sum(out.cpu().numpy())
+    return _sum(out)
 
 
 def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
@@ -51,12 +54,12 @@ def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
     out = _lib.out_buf(4)
     _lib.check(lib.vr_minmax(a.data_ptr(), _lib.ptr(b), _n(a), _lib.scratch().data_ptr(), out.data_ptr(),
                              _lib.stream()), "vr_minmax")
-    o = out.cpu().numpy()
     ctx = _dist.current()
     if ctx is not None:
-        m = ctx.allreduce(np.array([-o[0], o[1], -o[2], o[3]]), "max")
-        o = np.array([-m[0], m[1], -m[2], m[3]])
-    return o
+        out[0::2].neg_()
+        ctx.allreduce_(out, "max")
+        out[0::2].neg_()
+    return out.cpu().numpy()
 
 
 def local_absmax(x: torch.Tensor) -> float:
@@ -79,12 +82,11 @@ def vecstats(v: torch.Tensor) -> tuple:
     out = _lib.out_buf(4)
     _lib.check(lib.vr_vecstats(v.data_ptr(), _n(v) // 3, _lib.scratch().data_ptr(), out.data_ptr(),
                                _lib.stream()), "vr_vecstats")
-    o = out.cpu().numpy()
     ctx = _dist.current()
     if ctx is not None:
-        mx = ctx.allreduce(o[1:2], "max")[0]
-        cnt = ctx.allreduce(o[2:4], "sum")
-        o = np.array([o[0], mx, cnt[0], cnt[1]])
+        ctx.allreduce_(out[1:2], "max")
+        ctx.allreduce_(out[2:4], "sum")
+    o = out.cpu().numpy()
     return float(o[1]), int(o[2]), int(o[3])
 
 

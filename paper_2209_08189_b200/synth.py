@@ -70,9 +70,10 @@ def transport_labels(labels: LabelMap, v: VectorField, cfg: TransportConfig,
                 if j < cfg.n_t - 1:
                     cur = ops.sweep(cur, ops.forward.displacement, out=bufs[j % 2])
                 else:
-                    ext = ops.ctx.halo(cur, ops.w)
-                    _lib.check(lib.vr_label_step_slab(ext.data_ptr(), int(lab), d, ops.w, disp, order, None,
-                                                      out.data_ptr(), st), "vr_label_step_slab")
+                    lo, hi = ops.ctx.ghosts(cur, ops.w)
+                    _lib.check(lib.vr_label_step_slab(cur.data_ptr(), lo.data_ptr(), hi.data_ptr(), int(lab), d,
+                                                      ops.w, disp, order, None, out.data_ptr(), st),
+                               "vr_label_step_slab")
         return LabelMap(labels.grid, out)
     for lab in labels.label_ids():
         src = None

@@ -12,8 +12,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-import ctypes as C
-
 import torch
 
 from . import _lib
@@ -151,22 +149,17 @@ class TransportOperators:
         vmax1 = float(ctx.allreduce([local_absmax(v[0])], "max")[0])
         self.w = _dist.ghost_width(vmax1, cfg.dt, self.grid.dims[0], cfg.interp_order)
         ldims = ctx.local_dims
-        v_ext = ctx.halo(v, self.w)
-        self.div = torch.empty(ldims, dtype=torch.float32, device=v.device)
-        lib = _lib.lib()
-        st = _lib.stream()
-        _lib.check(lib.vr_fd8_div_slab(v_ext.data_ptr(), _lib.dims_arg(ldims), self.w, ctx.dims[0],
-                                       self.div.data_ptr(), st), "vr_fd8_div_slab")
-        div_ext = ctx.halo(self.div, self.w)
+        self.div = fd8_divergence_t(v)
+        v_ext = ctx.halo(v, self.w)          # contiguous ghost-extended copies, once per iterate
+        d_ext = ctx.halo(self.div, self.w)
         disp_f = torch.empty_like(v)
         disp_b = torch.empty_like(v)
         self.jac_factor = torch.empty_like(self.div)
         self.adj_factor = torch.empty_like(self.div)
-        dims4 = (C.c_int64 * 4)(*ldims, ctx.dims[0])
-        _lib.check(lib.vr_trace_rk2_slab(v_ext.data_ptr(), dims4, self.w, float(cfg.dt), _order(cfg.interp_order),
-                                         disp_f.data_ptr(), disp_b.data_ptr(), div_ext.data_ptr(),
-                                         self.jac_factor.data_ptr(), self.adj_factor.data_ptr(), st),
-                   "vr_trace_rk2_slab")
+        _lib.check(_lib.lib().vr_trace_rk2_slab(v_ext.data_ptr(), _lib.dims_arg(ldims), ctx.dims[0], self.w,
+                                                float(cfg.dt), _order(cfg.interp_order), disp_f.data_ptr(),
+                                                disp_b.data_ptr(), d_ext.data_ptr(), self.jac_factor.data_ptr(),
+                                                self.adj_factor.data_ptr(), _lib.stream()), "vr_trace_rk2_slab")
         return disp_f, disp_b
 
     def sweep(self, values: torch.Tensor, disp: torch.Tensor, factor: torch.Tensor | None = None,
@@ -176,10 +169,11 @@ class TransportOperators:
             return advect(values, disp, self.cfg.interp_order, factor=factor, out=out, flag=flag)
         if out is None:
             out = torch.empty(values.shape, dtype=torch.float32, device=values.device)
-        ext = self.ctx.halo(values, self.w)
-        _lib.check(_lib.lib().vr_advect_slab(ext.data_ptr(), _lib.dims_arg(self.ctx.local_dims), self.w,
-                                             disp.data_ptr(), _lib.ptr(factor), _order(self.cfg.interp_order),
-                                             out.data_ptr(), _lib.ptr(flag), _lib.stream()), "vr_advect_slab")
+        lo, hi = self.ctx.ghosts(values, self.w)
+        _lib.check(_lib.lib().vr_advect_slab(values.data_ptr(), lo.data_ptr(), hi.data_ptr(),
+                                             _lib.dims_arg(self.ctx.local_dims), self.w, disp.data_ptr(),
+                                             _lib.ptr(factor), _order(self.cfg.interp_order), out.data_ptr(),
+                                             _lib.ptr(flag), _lib.stream()), "vr_advect_slab")
         return out
 
     def inc_step(self, u: torch.Tensor, vt: torch.Tensor, gnext: torch.Tensor, last: int, out: torch.Tensor,
@@ -193,10 +187,10 @@ class TransportOperators:
             rc = lib.vr_incstate_step(u.data_ptr(), dims, disp, vt.data_ptr(), gnext.data_ptr(), float(cfg.dt),
                                       _order(cfg.interp_order), last, out.data_ptr(), _lib.ptr(flag), _lib.stream())
         else:
-            ext = self.ctx.halo(u, self.w)
-            rc = lib.vr_incstate_step_slab(ext.data_ptr(), dims, self.w, disp, vt.data_ptr(), gnext.data_ptr(),
-                                           float(cfg.dt), _order(cfg.interp_order), last, out.data_ptr(),
-                                           _lib.ptr(flag), _lib.stream())
+            lo, hi = self.ctx.ghosts(u, self.w)
+            rc = lib.vr_incstate_step_slab(u.data_ptr(), lo.data_ptr(), hi.data_ptr(), dims, self.w, disp,
+                                           vt.data_ptr(), gnext.data_ptr(), float(cfg.dt), _order(cfg.interp_order),
+                                           last, out.data_ptr(), _lib.ptr(flag), _lib.stream())
         _lib.check(rc, "vr_incstate_step")
 
     def advect_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:

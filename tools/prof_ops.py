@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--ops", default="spec_A,spec_inv,spec_K,advect_cubic,advect_linear,trace_cubic,fd8_grad,"
                                       "fd8_div,body,incstep,dots,h1")
+    ap.add_argument("--slab", action="store_true", help="also time the x1-slab kernels at world size 1")
     args = ap.parse_args()
     import paper_2209_08189_b200 as P
     from paper_2209_08189_b200 import _lib, transport, reductions
@@ -60,8 +61,31 @@ def main():
         "dots": (lambda: reductions.dots([(w, w), (w, out3)]), 3 * N * 4 * 3),
         "h1": (lambda: ws.h1_energy(f), N * 4),
     }
+    names = args.ops.split(",")
+    if args.slab:
+        import torch.distributed as tdist
+        from paper_2209_08189_b200 import dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        ctx = dist.SlabContext(g.dims)
+        with dist.activate(ctx):
+            tcs = P.TransportOperators(v, P.TransportConfig(4, "cubic"))
+        vlo, vhi = ctx.ghosts(v.data, tcs.w)
+        dlo, dhi = ctx.ghosts(tcs.div, tcs.w)
+        flo, fhi = ctx.ghosts(f, tcs.w)
+        dims_l = _lib.dims_arg(g.dims)
+        vext = ctx.halo(v.data, tcs.w)
+        dext = ctx.halo(tcs.div, tcs.w)
+        table["trace_cubic_slab"] = (lambda: _lib.lib().vr_trace_rk2_slab(
+            vext.data_ptr(), dims_l, n, tcs.w, 0.25, 3, out3.data_ptr(), w.data_ptr(), dext.data_ptr(),
+            out1.data_ptr(), f.data_ptr(), _lib.stream()), N * 48)
+        table["advect_cubic_slab"] = (lambda: _lib.lib().vr_advect_slab(
+            f.data_ptr(), flo.data_ptr(), fhi.data_ptr(), dims_l, tcs.w, tcs.forward.displacement.data_ptr(), None,
+            3, out1.data_ptr(), None, _lib.stream()), N * 20)
+        names += ["trace_cubic_slab", "advect_cubic_slab"]
     res = {}
-    for name in args.ops.split(","):
+    for name in names:
         fn, nbytes = table[name]
         fn()
         torch.cuda.synchronize()
