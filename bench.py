@@ -8,11 +8,13 @@ cubic, n_t=4, beta_v=1e-2, beta_w=0, GN-PCG to gtol 5e-2; one step = one full
 `register()` call from pinned host buffers incl. label transport + Dice and
 the velocity/deformed-image read-back (e2e).  Synthetic data.
 
-N > 1: the SAME registration decomposed into x1 slabs over N GPUs (strong
-scaling; dist.py: NCCL halo exchange for the SL / FD8 stencils, all-to-all
-transposes for the spectral operators, allreduce of the PCG/GN scalars),
-max-over-ranks device time.  --n / --order / --nt / --beta-w select other
-sizes, e.g. the C3 shape `--n 1024 --order linear --nt 16 --beta-w 1e-4`.
+N > 1 (default, "weak"): every GPU keeps a 256^3 block of one registration on
+the x1-extended lattice (256*N, 256, 256) -- the same C2 generator -- decomposed
+into x1 slabs (dist.py: NCCL halo exchange for the SL / FD8 stencils, one
+all-to-all per spectral transpose, allreduce of the PCG/GN scalars),
+max-over-ranks device time.  --strong decomposes the fixed N=1 problem instead.
+--n / --order / --nt / --beta-w select other sizes, e.g. the C3 shape
+`--n 1024 --order linear --nt 16 --beta-w 1e-4` (cubic lattice, strong).
 
 --impl reference: the CPU oracle (oracle/velreg_oracle.py, numpy + numba, all
 host threads) on a bounded sample of the same workload (one objective
@@ -52,6 +54,7 @@ def parse():
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--beta-w", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true", help="N>1: decompose the N=1 problem (strong scaling)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     return ap.parse_args()
 
@@ -219,7 +222,8 @@ def run_ours(args):
 
     from paper_2209_08189_b200 import dist as pdist
     n = args.n
-    g = P.make_grid((n, n, n))
+    weak = ws > 1 and not args.strong and args.n == 256
+    g = P.make_grid((n * ws, n, n) if weak else (n, n, n))
     cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=args.beta_w, n_t=args.nt, interp_order=args.order)
     slab = pdist.SlabContext(g.dims) if ws > 1 else None
     act = pdist.activate(slab)
@@ -239,6 +243,7 @@ def run_ours(args):
     dominant = "vr_advect"
     if ws > 1:
         dominant = "vr_advect_slab"
+    scaling = "weak" if (weak or ws == 1) else "strong"
     _lib.PROFILE.reset(timed=(dominant, "vr_spec_apply", "vr_trace_rk2", "vr_fd8_grad", "vr_trace_rk2_slab",
                               "vr_dspec_forward", "vr_dspec_xpass", "vr_dspec_inverse", "vr_fd8_grad_slab",
                               "vr_incstate_step_slab", "vr_incstate_step", "vr_body_force", "dist.ghosts",
@@ -323,10 +328,11 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32 (f64 reductions / forward spectra)", "data": "synthetic",
-            "config": {"workload": f"C2 sphere->deformed sphere {n}^3 GN-PCG, {args.order}, n_t={args.nt}, "
-                                   f"beta_v=1e-2, beta_w={args.beta_w:g}, gtol=5e-2",
+            "config": {"workload": f"C2 sphere->deformed sphere {'x'.join(map(str, g.dims))} GN-PCG, {args.order}, "
+                                   f"n_t={args.nt}, beta_v=1e-2, beta_w={args.beta_w:g}, gtol=5e-2"
+                                   + (f" (weak scaling: 256^3 per GPU)" if weak else ""),
                        "parallelism": f"x1-slab x{ws} (NCCL halo / all-to-all / allreduce)" if ws > 1 else "single",
                        "l2": "256 MB buffer written between timed steps; working set > 126 MB L2",
                        "gn_iterations": diag.gn_iterations,

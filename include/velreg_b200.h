@@ -175,10 +175,10 @@ int vr_fd8_div_slab(const float* v3, const float* v1_lo, const float* v1_hi, con
 int vr_spec_plan_is_fast(const vr_spec_plan* plan);
 int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, void* sendbuf, void* stream);
 int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
-                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, const void* recv, void* xout,
-                   void* stream);
-int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, double scale, double* out_dev,
-                        void* stream);
+                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, int l1, const void* recv,
+                   void* xout, void* stream);
+int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, int l1, double scale,
+                        double* out_dev, void* stream);
 int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
                      void* stream);
 

@@ -63,8 +63,8 @@ _SIGS = {
     "vr_fd8_div_slab": [_p, _p, _p, _dims_t, _i64, _p, _p],
     "vr_spec_plan_is_fast": [_p],
     "vr_dspec_forward": [_p, _p, _i32, _i32, _i32, _p, _p],
-    "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _p, _p, _p],
-    "vr_dspec_h1_partial": [_p, _p, _i32, _i32, _f64, _p, _p],
+    "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _i32, _p, _p, _p],
+    "vr_dspec_h1_partial": [_p, _p, _i32, _i32, _i32, _f64, _p, _p],
     "vr_dspec_inverse": [_p, _p, _i32, _i32, _p, _p, _p],
 }
 

@@ -207,6 +207,12 @@ struct SpecOp {
   int ncomp;
   double beta_v, beta_w, shift, scale, sigma;
   int j0, n2g;   // x2 offset / global x2 size of this tile (distributed transposed X pass)
+  int xblk;      // x1 rows per rank block: element (c, x1 = p*xblk + i) lives at
+                 // ((p*ncomp + c)*xblk + i) * lstride  (xblk = n1 for a single domain)
+  __host__ __device__ int64_t xoff(int c, int i, int64_t lstride) const {
+    const int p = i / xblk;
+    return ((int64_t)(p * ncomp + c) * xblk + (i - p * xblk)) * lstride;
+  }
 };
 
 __device__ __forceinline__ int signed_freq(int m, int n) { return m < n / 2 ? m : m - n; }  // fftfreq*n
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(256) x_op_kernel(const double2* __restrict__ S
     const int c = t / (L * nb);
     const int r = t - c * L * nb;
     const int i = r / nb, q = r - i * nb;
-    a[(c * B + q) * ls + i] = sbase[c * cstride + i * lstride + q];
+    a[(c * B + q) * ls + i] = sbase[op.xoff(c, i, lstride) + q];
   }
   // unused lines (q >= nb) are left untouched; they never reach memory
   __syncthreads();
@@ -432,7 +438,7 @@ __global__ void __launch_bounds__(256) x_op_kernel(const double2* __restrict__ S
     const int r = t - c * L * nb;
     const int i = r / nb, q = r - i * nb;
     const double2 v = out[(c * B + q) * ls + i];
-    tbase[c * cstride + i * lstride + q] = make_float2((float)v.x, (float)v.y);
+    tbase[op.xoff(c, i, lstride) + q] = make_float2((float)v.x, (float)v.y);
   }
 }
 
@@ -838,7 +844,7 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   const bool f64 = needs_f64(kind);
   int rc = spec_forward(p, in, ncomp, s, f64);
   if (rc) return rc;
-  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma, 0, d.n2};
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma, 0, d.n2, d.n1};
   spec_xpass(p, op, false, s, f64);
   spec_inverse_yz(p, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
@@ -872,7 +878,7 @@ int vr_h1_energy(vr_spec_plan* p, const float* f, double* out_dev, void* stream)
   const Dims& d = p->d;
   int rc = spec_forward(p, f, 1, s);
   if (rc) return rc;
-  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, 0, d.n2};
+  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, 0, d.n2, d.n1};
   const int nblk = spec_xpass(p, op, true, s);
   const double n = (double)d.n();
   finalize_sum_kernel<<<1, 1024, 0, s>>>(p->partials, nblk, kTwoPi * kTwoPi * kTwoPi / (n * n), out_dev);
@@ -908,13 +914,13 @@ __global__ void pack_kernel(const C* __restrict__ S, C* __restrict__ out, int nc
   const int L2 = N2 / P;
   const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    // out layout [c][q][i][jl][kz]
+    // out layout [q][c][i][jl][kz]: one contiguous block per destination rank
     int64_t r = e;
     const int kz = (int)(r % n3h); r /= n3h;
     const int jl = (int)(r % L2); r /= L2;
     const int i = (int)(r % L1); r /= L1;
-    const int q = (int)(r % P);
-    const int c = (int)(r / P);
+    const int c = (int)(r % ncomp);
+    const int q = (int)(r / ncomp);
     out[e] = S[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz];
   }
 }
@@ -924,13 +930,13 @@ __global__ void unpack_kernel(const float2* __restrict__ in, float2* __restrict_
   const int L2 = N2 / P;
   const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    // in layout [c][q][i][jl][kz]
+    // in layout [q][c][i][jl][kz]
     int64_t r = e;
     const int kz = (int)(r % n3h); r /= n3h;
     const int jl = (int)(r % L2); r /= L2;
     const int i = (int)(r % L1); r /= L1;
-    const int q = (int)(r % P);
-    const int c = (int)(r / P);
+    const int c = (int)(r % ncomp);
+    const int q = (int)(r / ncomp);
     T[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz] = in[e];
   }
 }
@@ -940,7 +946,7 @@ __global__ void unpack_kernel(const float2* __restrict__ in, float2* __restrict_
 extern "C" {
 
 // Z + Y forward passes of `in` (local slab, ncomp components) and pack into
-// sendbuf ([c][q][i][jl][kz], complex128 if f64 else complex64).
+// sendbuf ([q][c][i][jl][kz], complex128 if f64 else complex64).
 int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, void* sendbuf, void* stream) {
   if (!pl || !in || !sendbuf || nranks < 1 || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
@@ -960,26 +966,27 @@ int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int 
 }
 
 // X pass on the transposed block (px dims = {N1, L2, N3}); recv / xout are
-// [c][x1][jl][kz]; n_global = N1*N2*N3 for the inverse normalisation.
+// [p][c][il][jl][kz] (x1 = p*L1 + il: what one all-to-all delivers / sends);
+// n_global = N1*N2*N3 for the inverse normalisation.
 int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
-                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, const void* recv, void* xout,
-                   void* stream) {
-  if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+                   double sigma, double alpha, int64_t n_global, int j0, int n2_global, int l1, const void* recv,
+                   void* xout, void* stream) {
+  if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3) || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
   if (!px->fast) return VR_ERR_UNSUPPORTED;
-  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global};
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
   spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, reinterpret_cast<float2*>(xout));
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
 
 // H1 partial sum over this rank's transposed block -> *out_dev = scale * sum
-int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, double scale, double* out_dev,
-                        void* stream) {
-  if (!px || !recv || !out_dev) return VR_ERR_ARG;
+int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, int l1, double scale,
+                        double* out_dev, void* stream) {
+  if (!px || !recv || !out_dev || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   if (!px->fast) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
-  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, j0, n2_global};
+  SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, j0, n2_global, l1};
   const int nblk = spec_xpass(px, op, true, s, true, recv, nullptr);
   finalize_sum_kernel<<<1, 1024, 0, s>>>(px->partials, nblk, scale, out_dev);
   VR_CHECK_LAUNCH();

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(NC == 3 ? 384 : 256, NC == 3 ? 2 : 3) xop_fast
     const int e = threadIdx.x + u * NT;       // e = (c*L + i)*B + q
     const int q = e % B, ci = e / B;
     const int c = ci / L, i = ci - c * L;
-    x[u] = (q < nb) ? sbase[c * nspec + i * lstride + q] : mk<CF>(0.0, 0.0);
+    x[u] = (q < nb) ? sbase[op.xoff(c, i, lstride) + q] : mk<CF>(0.0, 0.0);
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NC == 3 ? 384 : 256, NC == 3 ? 2 : 3) xop_fast
       const int c = ci / L, i = ci - c * L;
       if (q < nb) {
         const CF v = tile[(c * B + q) * PL + padi(i)];
-        tbase[c * nspec + i * lstride + q] = make_float2((float)v.x, (float)v.y);
+        tbase[op.xoff(c, i, lstride) + q] = make_float2((float)v.x, (float)v.y);
       }
     }
   }

@@ -117,9 +117,9 @@ class DistSpectralWorkspace:
         self.device = torch.cuda.current_device()
 
     def _exchange(self, dst: torch.Tensor, src: torch.Tensor, ncomp: int, cplx_words: int) -> None:
-        m = self.per_comp * cplx_words
-        for c in range(ncomp):
-            self.ctx.alltoall(dst[c * m:(c + 1) * m], src[c * m:(c + 1) * m])
+        """One all-to-all for all components: blocks are [rank][component][...]."""
+        m = self.per_comp * cplx_words * ncomp
+        self.ctx.alltoall(dst[:m], src[:m])
 
     def apply(self, kind: int, x: torch.Tensor, out: torch.Tensor | None = None, add: torch.Tensor | None = None,
               beta_v: float = 0.0, beta_w: float = 0.0, shift: float = 0.0, sigma: float = 0.0,
@@ -139,8 +139,8 @@ class DistSpectralWorkspace:
         n1, n2, n3 = self.grid.dims
         _lib.check(lib.vr_dspec_xpass(self._px, int(kind), ncomp, int(f64), float(beta_v), float(beta_w),
                                       float(shift), float(sigma), float(alpha), n1 * n2 * n3,
-                                      self.ctx.rank * self.ctx.L2, n2, self.recv.data_ptr(), self.xout.data_ptr(),
-                                      st), "vr_dspec_xpass")
+                                      self.ctx.rank * self.ctx.L2, n2, self.ctx.L1, self.recv.data_ptr(),
+                                      self.xout.data_ptr(), st), "vr_dspec_xpass")
         self._exchange(self.irecv, self.xout, ncomp, 2)
         _lib.check(lib.vr_dspec_inverse(self._pl, self.irecv.data_ptr(), ncomp, P, _lib.ptr(add), out.data_ptr(),
                                         st), "vr_dspec_inverse")
@@ -156,7 +156,7 @@ class DistSpectralWorkspace:
         n = float(np.prod(self.grid.dims))
         out = _lib.out_buf(1)
         _lib.check(lib.vr_dspec_h1_partial(self._px, self.recv.data_ptr(), self.ctx.rank * self.ctx.L2,
-                                           self.grid.dims[1], TWO_PI ** 3 / (n * n), out.data_ptr(), st),
+                                           self.grid.dims[1], self.ctx.L1, TWO_PI ** 3 / (n * n), out.data_ptr(), st),
                    "vr_dspec_h1_partial")
         return float(self.ctx.allreduce(out.cpu().numpy(), "sum")[0])
 

@@ -70,28 +70,26 @@ def _halo_case(rank, world):
 
 
 def _transpose_case(rank, world):
-    """pack([c][q][i][jl][kz]) -> all-to-all -> [c][x1][jl][kz] complete x1 lines
-    (the contract of vr_dspec_forward / vr_dspec_xpass / vr_dspec_inverse)."""
+    """pack([q][c][i][jl][kz]) -> ONE all-to-all -> [p][c][il][jl][kz], i.e. complete
+    x1 lines x1 = p*L1 + il (the contract of vr_dspec_forward / vr_dspec_xpass /
+    vr_dspec_inverse)."""
     from paper_2209_08189_b200.dist import SlabContext
     ctx = SlabContext(DIMS)
     n1, n2, n3h = DIMS
     spec = np.random.default_rng(0).standard_normal((3, n1, n2, n3h)).astype(np.float32)
     loc = spec[:, ctx.x0:ctx.x0 + ctx.L1]
-    send = np.stack([loc[:, :, q * ctx.L2:(q + 1) * ctx.L2] for q in range(world)], axis=1)  # [c][q][i][jl][kz]
+    send = np.stack([loc[:, :, q * ctx.L2:(q + 1) * ctx.L2] for q in range(world)], axis=0)  # [q][c][i][jl][kz]
     send = torch.from_numpy(np.ascontiguousarray(send)).reshape(-1)
     recv = torch.empty_like(send)
-    m = ctx.L1 * n2 * n3h
-    for c in range(3):
-        ctx.alltoall(recv[c * m:(c + 1) * m], send[c * m:(c + 1) * m])
-    got = recv.reshape(3, n1, ctx.L2, n3h).numpy()
-    np.testing.assert_array_equal(got, spec[:, :, rank * ctx.L2:(rank + 1) * ctx.L2])
-    # inverse direction: [c][x1][jl][kz] blocks of x1 back to their owners
-    back = torch.empty_like(recv)
-    for c in range(3):
-        ctx.alltoall(back[c * m:(c + 1) * m], recv[c * m:(c + 1) * m])
-    got = back.reshape(3, world, ctx.L1, ctx.L2, n3h).numpy()      # [c][q][i][jl][kz]
-    want = np.stack([loc[:, :, q * ctx.L2:(q + 1) * ctx.L2] for q in range(world)], axis=1)
+    ctx.alltoall(recv, send)
+    got = recv.reshape(world, 3, ctx.L1, ctx.L2, n3h).numpy()      # [p][c][il][jl][kz]
+    want = spec[:, :, rank * ctx.L2:(rank + 1) * ctx.L2].reshape(3, world, ctx.L1, ctx.L2, n3h).transpose(1, 0, 2, 3, 4)
     np.testing.assert_array_equal(got, want)
+    # inverse direction: the X pass output keeps that layout; blocks go back to their owners
+    back = torch.empty_like(recv)
+    ctx.alltoall(back, recv)
+    got = back.reshape(world, 3, ctx.L1, ctx.L2, n3h).numpy()      # [q][c][i][jl][kz]
+    np.testing.assert_array_equal(got, send.reshape(world, 3, ctx.L1, ctx.L2, n3h).numpy())
 
 
 def _reduce_case(rank, world):
