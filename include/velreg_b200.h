@@ -152,12 +152,15 @@ int vr_label_counts(const int* l0, const int* l1, int64_t n, int max_id, unsigne
 int vr_trace_rk2_slab(const float* v_ext, const int64_t dims[3], int64_t n1_global, int w, double dt, int order,
                       float* disp_fwd, float* disp_bwd, const float* div_ext, float* fac_jac, float* fac_adj,
                       void* stream);
+/* sweeps on a slab cover output planes [x_begin, x_begin + x_count): planes
+ * [w, L1 - w) never touch the ghosts, so the host sweeps them while the ghost
+ * exchange is in flight and the 2w boundary planes afterwards */
 int vr_advect_slab(const float* src, const float* src_lo, const float* src_hi, const int64_t dims[3], int w,
-                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag,
-                   void* stream);
+                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag, int x_begin,
+                   int x_count, void* stream);
 int vr_incstate_step_slab(const float* u, const float* u_lo, const float* u_hi, const int64_t dims[3], int w,
                           const float* disp_fwd, const float* vt, const float* gradm_next, double dt, int order,
-                          int last, float* out, int* nonfinite_flag, void* stream);
+                          int last, float* out, int* nonfinite_flag, int x_begin, int x_count, void* stream);
 int vr_label_step_slab(const float* src, const float* src_lo, const float* src_hi, int label_id,
                        const int64_t dims[3], int w, const float* disp, int order, float* dst, int* labels_out,
                        void* stream);

@@ -56,8 +56,8 @@ _SIGS = {
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
     # x1-slab / distributed
     "vr_trace_rk2_slab": [_p, _dims_t, _i64, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
-    "vr_advect_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _i32, _p, _p, _p],
-    "vr_incstate_step_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
+    "vr_advect_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _i32, _p, _p, _i32, _i32, _p],
+    "vr_incstate_step_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _p, _f64, _i32, _i32, _p, _p, _i32, _i32, _p],
     "vr_label_step_slab": [_p, _p, _p, _i32, _dims_t, _i32, _p, _i32, _p, _p, _p],
     "vr_fd8_grad_slab": [_p, _p, _p, _dims_t, _i64, _p, _p],
     "vr_fd8_div_slab": [_p, _p, _p, _dims_t, _i64, _p, _p],

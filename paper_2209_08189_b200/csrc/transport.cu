@@ -25,17 +25,19 @@ struct Vox {
   int i, j, k, idx;
   bool ok;
 };
-__device__ __forceinline__ Vox vox3(const Dims& d) {
+__device__ __forceinline__ Vox vox3(const Dims& d, int x0 = 0) {
   Vox v;
   v.k = blockIdx.x * blockDim.x + threadIdx.x;
   v.j = blockIdx.y;
-  v.i = blockIdx.z;
+  v.i = blockIdx.z + x0;   // x0: first x1 plane of a partial (interior / boundary) launch
   v.ok = v.k < d.n3;
   v.idx = (v.i * d.n2 + v.j) * d.n3 + v.k;
   return v;
 }
 inline int vox_tpb(const Dims& d) { return d.n3 >= 128 ? 128 : ((d.n3 + 31) / 32) * 32; }
-inline dim3 vox_grid(const Dims& d) { return dim3((d.n3 + vox_tpb(d) - 1) / vox_tpb(d), d.n2, d.n1); }
+inline dim3 vox_grid(const Dims& d, int nplanes = -1) {
+  return dim3((d.n3 + vox_tpb(d) - 1) / vox_tpb(d), d.n2, nplanes < 0 ? d.n1 : nplanes);
+}
 
 __device__ __forceinline__ void flag_nonfinite(int* flag, float v) {
   if (flag && !isfinite(v)) atomicOr(flag, 1);
@@ -132,9 +134,9 @@ __global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v,
 template <int ORDER, bool SCALE, bool SLAB>
 __global__ void __launch_bounds__(128) advect_kernel(PlaneSrc<1, SLAB> src, Dims d, const float* __restrict__ disp,
                                                      const float* __restrict__ fac, float* __restrict__ dst,
-                                                     int* flag) {
+                                                     int* flag, int x0) {
   const int64_t N = d.n();
-  const Vox p = vox3(d);
+  const Vox p = vox3(d, x0);
   if (!p.ok) return;
   const int idx = p.idx;
   float o;
@@ -167,9 +169,9 @@ __global__ void __launch_bounds__(128) incstate_step_kernel(PlaneSrc<1, SLAB> u,
                                                             const float* __restrict__ disp,
                                                             const float* __restrict__ vt,
                                                             const float* __restrict__ gnext, float half,
-                                                            int last, float* __restrict__ out, int* flag) {
+                                                            int last, float* __restrict__ out, int* flag, int x0) {
   const int64_t N = d.n();
-  const Vox p = vox3(d);
+  const Vox p = vox3(d, x0);
   if (!p.ok) return;
   const int idx = p.idx;
   float o;
@@ -211,9 +213,10 @@ __global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict
 template <int ORDER, bool FROM_LABELS, bool TO_LABELS, bool SLAB>
 __global__ void __launch_bounds__(128) label_step_kernel(PlaneSrc<1, SLAB> src, const int* __restrict__ lab_in,
                                                          int id, Dims d, const float* __restrict__ disp,
-                                                         float* __restrict__ dst, int* __restrict__ lab_out) {
+                                                         float* __restrict__ dst, int* __restrict__ lab_out,
+                                                         int x0) {
   const int64_t N = d.n();
-  const Vox p = vox3(d);
+  const Vox p = vox3(d, x0);
   if (!p.ok) return;
   const int i = p.i, j = p.j, k = p.k, idx = p.idx;
   float o;
@@ -341,28 +344,31 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
 }
 
 static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], const float* disp, const float* factor,
-                       int order, float* dst, int* nonfinite_flag, void* stream) {
+                       int order, float* dst, int* nonfinite_flag, void* stream, int x0 = 0, int nx = -1) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!src || !disp || !dst || src == dst) return VR_ERR_ARG;
   if (sg.on() && (sg.w < 1 || sg.w > d.n1 || !sg.hi)) return VR_ERR_ARG;
+  if (nx < 0) nx = d.n1;
+  if (x0 < 0 || nx < 0 || x0 + nx > d.n1) return VR_ERR_ARG;
+  if (nx == 0) return VR_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const dim3 g = vox_grid(d);
+  const dim3 g = vox_grid(d, nx);
   const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
     if (sg.on()) {
       auto ps = slab_src<1>(src, sg.lo, sg.hi, 0, 0, sg.w, d.n1);
       if (factor)
-        advect_kernel<ORD, true, true><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag);
+        advect_kernel<ORD, true, true><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag, x0);
       else
-        advect_kernel<ORD, false, true><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag);
+        advect_kernel<ORD, false, true><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag, x0);
     } else {
       auto ps = full_src<1>(src, 0);
       if (factor)
-        advect_kernel<ORD, true, false><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag);
+        advect_kernel<ORD, true, false><<<g, tpb, 0, s>>>(ps, d, disp, factor, dst, nonfinite_flag, x0);
       else
-        advect_kernel<ORD, false, false><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag);
+        advect_kernel<ORD, false, false><<<g, tpb, 0, s>>>(ps, d, disp, nullptr, dst, nonfinite_flag, x0);
     }
   });
   VR_CHECK_LAUNCH();
@@ -371,22 +377,25 @@ static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], con
 
 static int incstate_impl(const float* u, SlabArgs sg, const int64_t dims[3], const float* disp_fwd, const float* vt,
                          const float* gradm_next, double dt, int order, int last, float* out, int* nonfinite_flag,
-                         void* stream) {
+                         void* stream, int x0 = 0, int nx = -1) {
   Dims d;
   int rc = dims_from(dims, &d);
   if (rc) return rc;
   if (!u || !disp_fwd || !vt || !gradm_next || !out || u == out) return VR_ERR_ARG;
   if (sg.on() && (sg.w < 1 || sg.w > d.n1 || !sg.hi)) return VR_ERR_ARG;
+  if (nx < 0) nx = d.n1;
+  if (x0 < 0 || nx < 0 || x0 + nx > d.n1) return VR_ERR_ARG;
+  if (nx == 0) return VR_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const dim3 g = vox_grid(d);
+  const dim3 g = vox_grid(d, nx);
   const int tpb = vox_tpb(d);
   VR_DISPATCH_ORDER(order, {
     if (sg.on())
       incstate_step_kernel<ORD, true><<<g, tpb, 0, s>>>(slab_src<1>(u, sg.lo, sg.hi, 0, 0, sg.w, d.n1), d, disp_fwd,
-                                                        vt, gradm_next, (float)(0.5 * dt), last, out, nonfinite_flag);
+                                                        vt, gradm_next, (float)(0.5 * dt), last, out, nonfinite_flag, x0);
     else
       incstate_step_kernel<ORD, false><<<g, tpb, 0, s>>>(full_src<1>(u, 0), d, disp_fwd, vt, gradm_next,
-                                                         (float)(0.5 * dt), last, out, nonfinite_flag);
+                                                         (float)(0.5 * dt), last, out, nonfinite_flag, x0);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -413,10 +422,11 @@ int vr_advect(const float* src, const int64_t dims[3], const float* disp, const 
 }
 
 int vr_advect_slab(const float* src, const float* src_lo, const float* src_hi, const int64_t dims[3], int w,
-                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag,
-                   void* stream) {
+                   const float* disp, const float* factor, int order, float* dst, int* nonfinite_flag, int x_begin,
+                   int x_count, void* stream) {
   if (!src_lo || !src_hi) return VR_ERR_ARG;
-  return advect_impl(src, SlabArgs{src_lo, src_hi, w}, dims, disp, factor, order, dst, nonfinite_flag, stream);
+  return advect_impl(src, SlabArgs{src_lo, src_hi, w}, dims, disp, factor, order, dst, nonfinite_flag, stream,
+                     x_begin, x_count);
 }
 
 int vr_incstate_init(const float* vt, const float* gradm0, const int64_t dims[3], double dt, float* u0,
@@ -440,10 +450,10 @@ int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fw
 
 int vr_incstate_step_slab(const float* u, const float* u_lo, const float* u_hi, const int64_t dims[3], int w,
                           const float* disp_fwd, const float* vt, const float* gradm_next, double dt, int order,
-                          int last, float* out, int* nonfinite_flag, void* stream) {
+                          int last, float* out, int* nonfinite_flag, int x_begin, int x_count, void* stream) {
   if (!u_lo || !u_hi) return VR_ERR_ARG;
   return incstate_impl(u, SlabArgs{u_lo, u_hi, w}, dims, disp_fwd, vt, gradm_next, dt, order, last, out,
-                       nonfinite_flag, stream);
+                       nonfinite_flag, stream, x_begin, x_count);
 }
 
 int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
@@ -472,14 +482,14 @@ int vr_label_step(const float* src, const int* labels_in, int label_id, const in
   VR_DISPATCH_ORDER(order, {
     if (from_l && to_l)
       label_step_kernel<ORD, true, true, false><<<g, tpb, 0, s>>>(ps, labels_in, label_id, d, disp, nullptr,
-                                                                  labels_out);
+                                                                  labels_out, 0);
     else if (from_l)
-      label_step_kernel<ORD, true, false, false><<<g, tpb, 0, s>>>(ps, labels_in, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, true, false, false><<<g, tpb, 0, s>>>(ps, labels_in, label_id, d, disp, dst, nullptr, 0);
     else if (to_l)
       label_step_kernel<ORD, false, true, false><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, nullptr,
-                                                                   labels_out);
+                                                                   labels_out, 0);
     else
-      label_step_kernel<ORD, false, false, false><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, false, false, false><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr, 0);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;
@@ -500,9 +510,9 @@ int vr_label_step_slab(const float* src, const float* src_lo, const float* src_h
   VR_DISPATCH_ORDER(order, {
     if (labels_out)
       label_step_kernel<ORD, false, true, true><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, nullptr,
-                                                                  labels_out);
+                                                                  labels_out, 0);
     else
-      label_step_kernel<ORD, false, false, true><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr);
+      label_step_kernel<ORD, false, false, true><<<g, tpb, 0, s>>>(ps, nullptr, label_id, d, disp, dst, nullptr, 0);
   });
   VR_CHECK_LAUNCH();
   return VR_OK;

@@ -131,6 +131,8 @@ class DistSpectralWorkspace:
             out = torch.empty_like(x)
         f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2)
         P = self.ctx.world
+        if ncomp == 3 and kind != _lib.SPEC_K and P > 1:
+            return self._apply_pipelined(kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha)
         _lib.check(lib.vr_dspec_forward(self._pl, x.data_ptr(), ncomp, int(f64), P, self.send.data_ptr(), st),
                    "vr_dspec_forward")
         snd = self.send if f64 else self.send.view(torch.float32)
@@ -144,6 +146,58 @@ class DistSpectralWorkspace:
         self._exchange(self.irecv, self.xout, ncomp, 2)
         _lib.check(lib.vr_dspec_inverse(self._pl, self.irecv.data_ptr(), ncomp, P, _lib.ptr(add), out.data_ptr(),
                                         st), "vr_dspec_inverse")
+        return out
+
+    def _apply_pipelined(self, kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha) -> torch.Tensor:
+        """Component-wise software pipeline: the all-to-all of one component is in
+        flight while the local passes / x1 pass of another run (K couples the
+        components inside the x1 pass and uses the fused path instead)."""
+        lib = _lib.lib()
+        st = _lib.stream()
+        P = self.ctx.world
+        n1, n2, n3 = self.grid.dims
+        nvox = x[0].numel()
+        esz = 16 if f64 else 8
+        blk = self.per_comp * esz                       # bytes of one component's spectrum
+        snd = self.send if f64 else self.send.view(torch.float32)
+        rcv = self.recv if f64 else self.recv.view(torch.float32)
+        words = blk // snd.element_size()
+        xwords = self.per_comp * 2                      # complex64 words per component
+
+        def fwd(c):
+            _lib.check(lib.vr_dspec_forward(self._pl, x.data_ptr() + 4 * c * nvox, 1, int(f64), P,
+                                            self.send.data_ptr() + c * blk, st), "vr_dspec_forward")
+            return self.ctx.alltoall(rcv[c * words:(c + 1) * words], snd[c * words:(c + 1) * words], async_op=True)
+
+        def xpass(c):
+            _lib.check(lib.vr_dspec_xpass(self._px, int(kind), 1, int(f64), float(beta_v), float(beta_w), float(shift),
+                                          float(sigma), float(alpha), n1 * n2 * n3, self.ctx.rank * self.ctx.L2, n2,
+                                          self.ctx.L1, self.recv.data_ptr() + c * blk,
+                                          self.xout.data_ptr() + 8 * c * self.per_comp, st), "vr_dspec_xpass")
+            return self.ctx.alltoall(self.irecv[c * xwords:(c + 1) * xwords], self.xout[c * xwords:(c + 1) * xwords],
+                                     async_op=True)
+
+        def inv(c):
+            a = None if add is None else add.data_ptr() + 4 * c * nvox
+            _lib.check(lib.vr_dspec_inverse(self._pl, self.irecv.data_ptr() + 8 * c * self.per_comp, 1, P, a,
+                                            out.data_ptr() + 4 * c * nvox, st), "vr_dspec_inverse")
+
+        with _lib.timed("dist.spectral"):
+            a0 = fwd(0)
+            a1 = fwd(1)
+            a0.wait()
+            b0 = xpass(0)
+            a2 = fwd(2)
+            a1.wait()
+            b1 = xpass(1)
+            b0.wait()
+            inv(0)
+            a2.wait()
+            b2 = xpass(2)
+            b1.wait()
+            inv(1)
+            b2.wait()
+            inv(2)
         return out
 
     def h1_energy(self, f: torch.Tensor) -> float:

@@ -96,9 +96,21 @@ class SlabContext:
         if self.world == 1:
             return send_hi.contiguous(), send_lo.contiguous()
         with _lib.timed("dist.ghosts"):
-            return self._exchange_ghosts(send_lo, send_hi)
+            lo, hi, works = self.ghosts_async(x, w)
+            self.finish(works)
+        return lo, hi
 
-    def _exchange_ghosts(self, send_lo, send_hi):
+    def ghosts_async(self, x: torch.Tensor, w: int) -> tuple:
+        """Post the ghost exchange and return (lo, hi, works) without waiting, so
+        the interior planes can be swept meanwhile; `finish(works)` makes the
+        current stream wait for the ghosts."""
+        L1 = x.shape[-3]
+        if w > L1:
+            raise ValueError(f"ghost width {w} exceeds the slab depth {L1}; use fewer ranks")
+        send_lo = x[..., :w, :, :]
+        send_hi = x[..., L1 - w:, :, :]
+        if self.world == 1:
+            return send_hi.contiguous(), send_lo.contiguous(), []
         send_lo = send_lo.contiguous()
         send_hi = send_hi.contiguous()
         hi = torch.empty_like(send_lo)        # <- right neighbour's first planes
@@ -107,9 +119,12 @@ class SlabContext:
                tdist.P2POp(tdist.isend, send_hi, self.right, self.group),
                tdist.P2POp(tdist.irecv, hi, self.right, self.group),
                tdist.P2POp(tdist.irecv, lo, self.left, self.group)]
-        for req in tdist.batch_isend_irecv(ops):
+        return lo, hi, tdist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def finish(works) -> None:
+        for req in works:
             req.wait()
-        return lo, hi
 
     def halo(self, x: torch.Tensor, w: int) -> torch.Tensor:
         """(..., L1, N2, N3) -> (..., L1 + 2w, N2, N3) extended copy (tests / tools)."""
@@ -117,13 +132,17 @@ class SlabContext:
         return torch.cat([lo, x, hi], dim=-3)
 
     # ---- transposes -------------------------------------------------------------
-    def alltoall(self, out: torch.Tensor, inp: torch.Tensor) -> None:
-        """Equal-split all-to-all along dim 0 of flat views (x1 slabs <-> x2 slabs)."""
+    def alltoall(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        """Equal-split all-to-all along dim 0 of flat views (x1 slabs <-> x2 slabs);
+        async_op returns the work handle (wait() = stream wait)."""
         if self.world == 1:
             out.copy_(inp)
-            return
+            return None
+        if async_op:
+            return tdist.all_to_all_single(out, inp, group=self.group, async_op=True)
         with _lib.timed("dist.alltoall"):
             tdist.all_to_all_single(out, inp, group=self.group)
+        return None
 
     # ---- synthetic-input helpers -------------------------------------------------
     def local_coords(self) -> np.ndarray:

@@ -169,12 +169,32 @@ class TransportOperators:
             return advect(values, disp, self.cfg.interp_order, factor=factor, out=out, flag=flag)
         if out is None:
             out = torch.empty(values.shape, dtype=torch.float32, device=values.device)
-        lo, hi = self.ctx.ghosts(values, self.w)
-        _lib.check(_lib.lib().vr_advect_slab(values.data_ptr(), lo.data_ptr(), hi.data_ptr(),
-                                             _lib.dims_arg(self.ctx.local_dims), self.w, disp.data_ptr(),
-                                             _lib.ptr(factor), _order(self.cfg.interp_order), out.data_ptr(),
-                                             _lib.ptr(flag), _lib.stream()), "vr_advect_slab")
+        dims = _lib.dims_arg(self.ctx.local_dims)
+        order = _order(self.cfg.interp_order)
+
+        def launch(lo, hi, x0, nx):
+            _lib.check(_lib.lib().vr_advect_slab(values.data_ptr(), lo.data_ptr(), hi.data_ptr(), dims, self.w,
+                                                 disp.data_ptr(), _lib.ptr(factor), order, out.data_ptr(),
+                                                 _lib.ptr(flag), x0, nx, _lib.stream()), "vr_advect_slab")
+
+        self._overlapped(values, launch)
         return out
+
+    def _overlapped(self, values: torch.Tensor, launch) -> None:
+        """Ghost exchange in flight while the interior planes [w, L1 - w) (whose
+        stencils never leave the slab) are swept; boundary planes afterwards."""
+        ctx, w = self.ctx, self.w
+        L1 = ctx.local_dims[0]
+        with _lib.timed("dist.sweep"):
+            lo, hi, works = ctx.ghosts_async(values, w)
+            if L1 > 2 * w:
+                launch(lo, hi, w, L1 - 2 * w)
+                ctx.finish(works)
+                launch(lo, hi, 0, w)
+                launch(lo, hi, L1 - w, w)
+            else:
+                ctx.finish(works)
+                launch(lo, hi, 0, L1)
 
     def inc_step(self, u: torch.Tensor, vt: torch.Tensor, gnext: torch.Tensor, last: int, out: torch.Tensor,
                  flag=None) -> None:
@@ -186,12 +206,15 @@ class TransportOperators:
         if self.ctx is None:
             rc = lib.vr_incstate_step(u.data_ptr(), dims, disp, vt.data_ptr(), gnext.data_ptr(), float(cfg.dt),
                                       _order(cfg.interp_order), last, out.data_ptr(), _lib.ptr(flag), _lib.stream())
+            _lib.check(rc, "vr_incstate_step")
         else:
-            lo, hi = self.ctx.ghosts(u, self.w)
-            rc = lib.vr_incstate_step_slab(u.data_ptr(), lo.data_ptr(), hi.data_ptr(), dims, self.w, disp,
-                                           vt.data_ptr(), gnext.data_ptr(), float(cfg.dt), _order(cfg.interp_order),
-                                           last, out.data_ptr(), _lib.ptr(flag), _lib.stream())
-        _lib.check(rc, "vr_incstate_step")
+            def launch(lo, hi, x0, nx):
+                _lib.check(lib.vr_incstate_step_slab(u.data_ptr(), lo.data_ptr(), hi.data_ptr(), dims, self.w, disp,
+                                                     vt.data_ptr(), gnext.data_ptr(), float(cfg.dt),
+                                                     _order(cfg.interp_order), last, out.data_ptr(), _lib.ptr(flag),
+                                                     x0, nx, _lib.stream()), "vr_incstate_step_slab")
+
+            self._overlapped(u, launch)
 
     def advect_step(self, values: torch.Tensor, out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
         return self.sweep(values, self.forward.displacement, out=out, flag=flag)
