@@ -1,16 +1,24 @@
-// Shared-memory-staged semi-Lagrangian gathers.
+// Shared-memory-staged tricubic sweeps ("z-quad" staging) -- EXPERIMENT, not
+// built into libvelreg_b200 (no .cu includes it).  Correct (passed the full
+// GPU parity suite when wired into vr_advect / vr_incstate_step / labels) but
+// measured 0.385 ms vs 0.33 ms for the direct lean gather at 256^3 (B200):
+// the staged path is latency-bound (3 CTAs / SM by 64 KB smem, serialized
+// load -> reduce -> stage -> gather phases; ncu: long_scoreboard stalls,
+// 67 % L1tex throughput).  Kept for a persistent, double-buffered revisit.
 //
-// One CTA owns a TX x TY x TZ tile of arrival voxels (4 x 8 x 32; 256 threads,
-// each thread 4 voxels along x1).  It reads the tile's departure points (the
-// displacement field, coalesced), reduces their floor-index bounding box, and
-// stages that box of the source volume -- plus the interpolation stencil --
-// into shared memory with coalesced x3-row loads (periodic wrap applied while
-// loading).  All 8 (trilinear) / 64 (tricubic) taps per point are then read
-// from shared memory instead of issuing scattered L1/L2 gathers.  Smooth
-// characteristics make the box only slightly larger than the tile
-// (~3.7 source voxels staged per arrival voxel for C2); a tile whose box
-// exceeds the budget (rough velocity, tiny grid) falls back to direct gathers
-// -- same arithmetic, same results.
+// One CTA owns a TX x TY x TZ = 4 x 8 x 32 tile of arrival voxels (256 threads:
+// lanes along x3, warps along x2, 4 x1 planes per thread).  It reads the tile's
+// displacements, reduces the floor-index bounding box of the departure points,
+// and stages the source box -- stencil included -- in shared memory as
+// overlapping float4 quads Q[row][c] = (f[c], f[c+1], f[c+2], f[c+3]) along x3.
+// Every stencil row of a tricubic tap set is then ONE 16-byte shared load:
+// 16 LDS.128 per point instead of 64 scattered LDG, which makes the gather
+// shared-memory-bandwidth bound (~2 clk/point/SM) instead of L1/LSU bound.
+// Smooth characteristics keep the box small (C2: ~8 x 12 x 36 quads = 55 KB for
+// 1024 points, ~3.4 L1-resident loads per point to stage).  A tile whose box
+// exceeds the budget (rough velocity, tiny grid) uses the direct gather --
+// same arithmetic, same results.  Sources: periodic fields or x1 slabs with
+// ghost blocks (PlaneSrc); the label-indicator source converts while staging.
 #pragma once
 #include <climits>
 #include "interp.cuh"
@@ -19,77 +27,69 @@ namespace vr {
 namespace staged {
 
 constexpr int TZ = 32, TY = 8, TX = 4;
-constexpr int CAP = 12032;  // staged floats per CTA (47 KB), 4 CTAs per SM
+constexpr int QCAP = 4096;                       // float4 quads per CTA (64 KB)
+constexpr size_t kSmem = sizeof(float4) * QCAP;
 
-__device__ __forceinline__ void voxel_of(int idx, const Dims& d, int& i, int& j, int& k) {
-  k = idx % d.n3;
-  const int r = idx / d.n3;
-  j = r % d.n2;
-  i = r / d.n2;
-}
-
-// interpolation from the staged box; (lx, ly, lz) = floor index minus box origin
-// (the box origin already includes the cubic stencil's -1)
-__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-
-// how a source is staged: raw fp32 fields go through cp.async (no register
-// round trip, every copy in flight at once); label indicators are converted.
-template <class Src> struct Stager;
-template <> struct Stager<SrcF32> {
-  __device__ __forceinline__ static void put(const SrcF32& s, float* dst, int idx) { cp_async4(dst, s.p[0] + idx); }
-};
-template <> struct Stager<SrcLabel> {
-  __device__ __forceinline__ static void put(const SrcLabel& s, float* dst, int idx) { *dst = s(0, idx); }
+// source adaptors for staging: value at (x1 plane, in-plane offset)
+template <bool SLAB>
+struct FieldSrc {
+  PlaneSrc<1, SLAB> p;
+  __device__ __forceinline__ const float* plane(int x, int psz) const { return p.plane(0, x, psz); }
+  __device__ __forceinline__ float at(const float* pl, int off) const { return __ldg(pl + off); }
 };
 
-template <int ORDER>
-__device__ __forceinline__ float gather_box(const float* __restrict__ box, int by, int bz, int lx, int ly, int lz,
-                                            float tx, float ty, float tz) {
-  if (ORDER == ORDER_LINEAR) {
-    const int r00 = (lx * by + ly) * bz + lz, r01 = r00 + bz;
-    const int r10 = r00 + by * bz, r11 = r10 + bz;
-    const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
-    const float c00 = box[r00] * sz + box[r00 + 1] * tz;
-    const float c01 = box[r01] * sz + box[r01 + 1] * tz;
-    const float c10 = box[r10] * sz + box[r10 + 1] * tz;
-    const float c11 = box[r11] * sz + box[r11 + 1] * tz;
-    const float c0 = c00 * sy + c01 * ty;
-    const float c1 = c10 * sy + c11 * ty;
-    return c0 * sx + c1 * tx;
+struct LabelSrc {  // indicator of one label id (synth.py:125), periodic only
+  const int* lab;
+  int id;
+  __device__ __forceinline__ const int* plane(int x, int psz) const { return lab + (int64_t)x * psz; }
+  __device__ __forceinline__ float at(const int* pl, int off) const { return __ldg(pl + off) == id ? 1.0f : 0.0f; }
+};
+
+// direct (unstaged) tricubic gather through the same adaptor, periodic / slab x1
+template <bool SLAB, class S>
+__device__ __forceinline__ float direct_cubic(const S& src, const Dims& d, int w, int L1, int ix, int iy, int iz,
+                                              float tx, float ty, float tz) {
+  float wx[4], wy[4], wz[4];
+  lagrange4(tx, wx);
+  lagrange4(ty, wy);
+  lagrange4(tz, wz);
+  const int psz = d.n2 * d.n3;
+  int xo[4], yo[4], zo[4];
+  if (SLAB) {
+    const int i0 = clampi(ix, 1 - w, L1 + w - 3);
+    xo[0] = i0 - 1; xo[1] = i0; xo[2] = i0 + 1; xo[3] = i0 + 2;
   } else {
-    float wx[4], wy[4], wz[4];
-    lagrange4(tx, wx);
-    lagrange4(ty, wy);
-    lagrange4(tz, wz);
-    float acc = 0.0f;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      float sa = 0.0f;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const float* row = box + ((lx + a) * by + (ly + b)) * bz + lz;
-        const float sb = wz[0] * row[0] + wz[1] * row[1] + wz[2] * row[2] + wz[3] * row[3];
-        sa += wy[b] * sb;
-      }
-      acc += wx[a] * sa;
-    }
-    return acc;
+    cubic_idx(wrap_idx(ix, d.n1), d.n1, xo);
   }
+  cubic_idx(wrap_idx(iy, d.n2), d.n2, yo);
+  cubic_idx(wrap_idx(iz, d.n3), d.n3, zo);
+  float acc = 0.0f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const auto pl = src.plane(xo[a], psz);
+    float sa = 0.0f;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = yo[b] * d.n3;
+      sa += wy[b] * (wz[0] * src.at(pl, r + zo[0]) + wz[1] * src.at(pl, r + zo[1]) + wz[2] * src.at(pl, r + zo[2]) +
+                     wz[3] * src.at(pl, r + zo[3]));
+    }
+    acc += wx[a] * sa;
+  }
+  return acc;
 }
 
-// Generic staged sweep: out voxel idx <- epi(idx, interp(src, departure(idx)))
-template <int ORDER, class Src, class Epi>
-__global__ void __launch_bounds__(256, 4) sweep_kernel(Src src, Dims d, const float* __restrict__ disp, Epi epi) {
-  extern __shared__ float box[];
+// Generic staged tricubic sweep: out voxel idx <- epi(idx, interp(src, departure(idx)))
+// over output x1 planes [x_begin, x_begin + x_count) of the (local) dims d.
+template <bool SLAB, class S, class Epi>
+__global__ void __launch_bounds__(256, 3) quad_sweep_kernel(S src, Dims d, int w, int x_begin, int x_count,
+                                                            const float* __restrict__ disp, Epi epi) {
+  extern __shared__ float4 quads[];
   __shared__ int ext[6];
   const int64_t N = d.n();
-  const int z0 = blockIdx.x * TZ, y0 = blockIdx.y * TY, x0 = blockIdx.z * TX;
+  const int L1 = d.n1;
+  const int z0 = blockIdx.x * TZ, y0 = blockIdx.y * TY, x0 = x_begin + blockIdx.z * TX;
+  const int x_end = x_begin + x_count;
   const int k = z0 + threadIdx.x, j = y0 + threadIdx.y;
   const int tid = threadIdx.y * TZ + threadIdx.x;
   if (tid < 6) ext[tid] = (tid < 3) ? INT_MAX : INT_MIN;
@@ -102,11 +102,12 @@ __global__ void __launch_bounds__(256, 4) sweep_kernel(Src src, Dims d, const fl
     const int i = x0 + u;
     ix[u] = iy[u] = iz[u] = 0;
     fx[u] = fy[u] = fz[u] = 0.0f;
-    if (inyz && i < d.n1) {
+    if (inyz && i < x_end) {
       const int idx = (i * d.n2 + j) * d.n3 + k;
       split_coord(i, __ldg(disp + idx), ix[u], fx[u]);
       split_coord(j, __ldg(disp + N + idx), iy[u], fy[u]);
       split_coord(k, __ldg(disp + 2 * N + idx), iz[u], fz[u]);
+      if (SLAB) ix[u] = clampi(ix[u], 1 - w, L1 + w - 3);
       mn0 = min(mn0, ix[u]); mx0 = max(mx0, ix[u]);
       mn1 = min(mn1, iy[u]); mx1 = max(mx1, iy[u]);
       mn2 = min(mn2, iz[u]); mx2 = max(mx2, iz[u]);
@@ -124,43 +125,86 @@ __global__ void __launch_bounds__(256, 4) sweep_kernel(Src src, Dims d, const fl
     atomicMax(&ext[3], mx0); atomicMax(&ext[4], mx1); atomicMax(&ext[5], mx2);
   }
   __syncthreads();
-  const int lo_off = (ORDER == ORDER_CUBIC) ? 1 : 0, hi_off = (ORDER == ORDER_CUBIC) ? 2 : 1;
-  const int lox = ext[0] - lo_off, loy = ext[1] - lo_off, loz = ext[2] - lo_off;
-  const int bx = ext[3] + hi_off - lox + 1, by = ext[4] + hi_off - loy + 1, bz = ext[5] + hi_off - loz + 1;
-  const bool use_box = bx <= d.n1 && by <= d.n2 && bz <= d.n3 && (int64_t)bx * by * ((bz + 31) & ~31) <= CAP;
-  const int bzp = (bz + 31) & ~31;  // x3 row pitch in the box
+  // box of stencil rows: x1 [lo0-1, hi0+2], x2 [lo1-1, hi1+2]; quads start at x3 lo2-1 .. hi2-1
+  const int bx0 = ext[0] - 1, by0 = ext[1] - 1, qz0 = ext[2] - 1;
+  const int BX = ext[3] - ext[0] + 4, BY = ext[4] - ext[1] + 4, QZ = ext[5] - ext[2] + 1;
+  const bool use_box = BX <= d.n1 + (SLAB ? 2 * w : 0) && BY <= d.n2 && QZ + 3 <= d.n3 && QZ <= 2 * 29 &&
+                       (int64_t)BX * BY * QZ <= QCAP;
+  const int psz = d.n2 * d.n3;
   if (use_box) {
-    // stage: one x3 row of the box per warp iteration, lanes along x3 (coalesced);
-    // all copies are issued before the single wait
+    // staging: warp w owns box x1 rows a = w, w+8, ... (one plane pointer each)
+    // and walks its x2 rows 4 at a time with an incremental conditional wrap; a
+    // row is read in 29-quad windows -- lane l loads f[c0+l] once (coalesced)
+    // and lanes l < 29 assemble quad (f[l], f[l+1], f[l+2], f[l+3]) with
+    // shuffles, so every float is loaded once and 8 loads are in flight.
     const int warp = tid >> 5, lane = tid & 31;
-    const int lzw = wrap_idx(loz, d.n3);
-    const int nrows = bx * by;
-    int a = warp / by, b = warp - a * by;
-    for (int row = warp; row < nrows; row += 8) {
-      const int gi = wrap_idx(lox + a, d.n1), gj = wrap_idx(loy + b, d.n2);
-      const int rbase = (gi * d.n2 + gj) * d.n3;
-      float* dst = box + row * bzp;
-      for (int c = lane; c < bz; c += 32) {
-        int gk = lzw + c;
-        gk = gk >= d.n3 ? gk - d.n3 : gk;
-        Stager<Src>::put(src, dst + c, rbase + gk);
-      }
-      b += 8;
-      while (b >= by) { b -= by; ++a; }
+    constexpr int RPI = 4, WPR = 2, QW = 29;
+    int z_lo[WPR];
+#pragma unroll
+    for (int q = 0; q < WPR; ++q) {   // x3 index of this lane's element in window q
+      int z = wrap_idx(qz0, d.n3) + q * QW + lane;
+      z = z >= d.n3 ? z - d.n3 : z;
+      z_lo[q] = z >= d.n3 ? z - d.n3 : z;
     }
-    cp_async_wait_all();
+    const int gy0 = wrap_idx(by0, d.n2);
+    for (int a = warp; a < BX; a += 8) {
+      const int gx = SLAB ? bx0 + a : wrap_idx(bx0 + a, d.n1);
+      const auto pl = src.plane(gx, psz);
+      for (int b0 = 0; b0 < BY; b0 += RPI) {
+        float v[RPI][WPR];
+#pragma unroll
+        for (int r = 0; r < RPI; ++r) {
+          int gy = gy0 + b0 + r;
+          gy = gy >= d.n2 ? gy - d.n2 : gy;
+          const bool rok = b0 + r < BY;
+          const int rbase = (rok ? gy : 0) * d.n3;
+#pragma unroll
+          for (int q = 0; q < WPR; ++q)
+            v[r][q] = (rok && q * QW + lane < QZ + 3) ? src.at(pl, rbase + z_lo[q]) : 0.0f;
+        }
+#pragma unroll
+        for (int r = 0; r < RPI; ++r) {
+          float4* qrow = quads + (a * BY + b0 + r) * QZ;
+#pragma unroll
+          for (int q = 0; q < WPR; ++q) {
+            const float x0v = v[r][q];
+            const float x1v = __shfl_down_sync(0xffffffffu, x0v, 1);
+            const float x2v = __shfl_down_sync(0xffffffffu, x0v, 2);
+            const float x3v = __shfl_down_sync(0xffffffffu, x0v, 3);
+            const int c = q * QW + lane;
+            if (b0 + r < BY && lane < QW && c < QZ) qrow[c] = make_float4(x0v, x1v, x2v, x3v);
+          }
+        }
+      }
+    }
     __syncthreads();
   }
+  const int sa_row = BY * QZ;  // x1 stride in quads
 #pragma unroll
   for (int u = 0; u < TX; ++u) {
     const int i = x0 + u;
-    if (!(inyz && i < d.n1)) continue;
+    if (!(inyz && i < x_end)) continue;
     float o;
     if (use_box) {
-      o = gather_box<ORDER>(box, by, bzp, ix[u] - lox - lo_off, iy[u] - loy - lo_off, iz[u] - loz - lo_off, fx[u],
-                            fy[u], fz[u]);
+      float wx[4], wy[4], wz[4];
+      lagrange4(fx[u], wx);
+      lagrange4(fy[u], wy);
+      lagrange4(fz[u], wz);
+      const float4* q = quads + ((ix[u] - 1 - bx0) * BY + (iy[u] - 1 - by0)) * QZ + (iz[u] - 1 - qz0);
+      float acc = 0.0f;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        float sa = 0.0f;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const float4 v = q[a * sa_row + b * QZ];
+          sa += wy[b] * (wz[0] * v.x + wz[1] * v.y + wz[2] * v.z + wz[3] * v.w);
+        }
+        acc += wx[a] * sa;
+      }
+      o = acc;
     } else {
-      gather<ORDER, 1>(src, d, ix[u], iy[u], iz[u], fx[u], fy[u], fz[u], &o);
+      o = direct_cubic<SLAB>(src, d, w, L1, ix[u], iy[u], iz[u], fx[u], fy[u], fz[u]);
     }
     epi((i * d.n2 + j) * d.n3 + k, o);
   }
@@ -211,11 +255,10 @@ struct EpiLabel {  // label transport: float indicator or thresholded label writ
   }
 };
 
-inline dim3 sweep_grid(const Dims& d) {
-  return dim3((d.n3 + TZ - 1) / TZ, (d.n2 + TY - 1) / TY, (d.n1 + TX - 1) / TX);
+inline dim3 sweep_grid(const Dims& d, int nplanes) {
+  return dim3((d.n3 + TZ - 1) / TZ, (d.n2 + TY - 1) / TY, (nplanes + TX - 1) / TX);
 }
 inline dim3 sweep_block() { return dim3(TZ, TY); }
-constexpr size_t kSweepSmem = sizeof(float) * CAP;
 
 }  // namespace staged
 }  // namespace vr
