@@ -17,6 +17,8 @@ from .errors import VelregError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvelreg_b200.so")
+# A/B experiments: load an alternative in-tree build (same C ABI)
+LIB_PATH = os.environ.get("VR_LIB_PATH", LIB_PATH)
 
 _lib = None
 _lock = threading.Lock()
@@ -220,6 +222,35 @@ def dims_arg(dims) -> C.Array:
 
 def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---- deferred non-finite checks ------------------------------------------------
+# The Hessian matvec's incremental-state and adjoint solves raise TransportError
+# on non-finite output like the reference (transport.py:119-121, :184, :156).
+# Reading their device flag right away would cost a host sync per solve; the
+# read is deferred to the next host read of a reduction (reductions._sum), which
+# PCG performs right after every matvec, so the error surfaces from the same
+# PCG iteration.
+_deferred: list = []
+
+
+def defer_check(flag: torch.Tensor, exc: Exception) -> None:
+    _deferred.append((flag, exc))
+
+
+def is_deferred(flag: torch.Tensor) -> bool:
+    return any(f is flag for f, _ in _deferred)
+
+
+def run_deferred() -> None:
+    if not _deferred:
+        return
+    items = list(_deferred)
+    _deferred.clear()
+    vals = torch.stack([f.reshape(()) for f, _ in items]).cpu().tolist()
+    for (_, exc), v in zip(items, vals):
+        if v:
+            raise exc
 
 
 # ---- per-device scratch for reductions -------------------------------------

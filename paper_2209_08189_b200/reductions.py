@@ -21,7 +21,9 @@ def _sum(out: torch.Tensor) -> np.ndarray:
     ctx = _dist.current()
     if ctx is not None:
         ctx.allreduce_(out, "sum")
-    return out.cpu().numpy()
+    res = out.cpu().numpy()
+    _lib.run_deferred()
+    return res
 
 
 def dots(pairs) -> np.ndarray:

@@ -137,7 +137,9 @@ class TransportOperators:
             disp_f, disp_b = self._trace_slab(v.data)
         self.forward = Characteristics(v.grid, disp_f, cfg.dt)
         self.backward = Characteristics(v.grid, disp_b, cfg.dt)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=v.data.device)
+        # non-finite flags: [0] eager checks, [1] / [2] the matvec's deferred
+        # incremental-state / adjoint checks
+        self.flags = torch.zeros((3, 1), dtype=torch.int32, device=v.data.device)
 
     # ---- x1-slab decomposition (dist.py) ----------------------------------------
     def _trace_slab(self, v: torch.Tensor):
@@ -223,13 +225,20 @@ class TransportOperators:
         return self.sweep(values, self.backward.displacement, out=out, flag=flag)
 
     # non-finite guard (transport.py:119-121) read back at the reference's check points
-    def arm(self) -> torch.Tensor:
-        self.flag.zero_()
-        return self.flag
+    def arm(self, slot: int = 0) -> torch.Tensor:
+        flag = self.flags[slot]
+        if _lib.is_deferred(flag):
+            _lib.run_deferred()
+        flag.zero_()
+        return flag
 
-    def raise_if_flagged(self, what: str) -> None:
-        if int(self.flag.item()) != 0:
-            raise TransportError(f"{what} produced non-finite values")
+    def raise_if_flagged(self, what: str, slot: int = 0, deferred: bool = False) -> None:
+        flag = self.flags[slot]
+        exc = TransportError(f"{what} produced non-finite values")
+        if deferred:
+            _lib.defer_check(flag, exc)
+        elif int(flag.item()) != 0:
+            raise exc
 
 
 def _ops_for(v: VectorField, cfg: TransportConfig, ops) -> TransportOperators:
@@ -284,12 +293,14 @@ def solve_adjoint(final_lambda: ScalarField, v: VectorField, cfg: TransportConfi
     return series
 
 
-def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: TransportConfig) -> None:
-    flag = ops.arm()
+def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: TransportConfig,
+                   deferred: bool = False) -> None:
+    slot = 2 if deferred else 0
+    flag = ops.arm(slot)
     for j in range(cfg.n_t - 1, -1, -1):
         ops.sweep(series[j + 1], ops.backward.displacement, factor=ops.adj_factor, out=series[j],
                   flag=flag if j == 0 else None)
-    ops.raise_if_flagged("adjoint solve")
+    ops.raise_if_flagged("adjoint solve", slot, deferred)
 
 
 def gradient_series(m_series: torch.Tensor) -> torch.Tensor:
@@ -302,7 +313,7 @@ def gradient_series(m_series: torch.Tensor) -> torch.Tensor:
 
 
 def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOperators, cfg: TransportConfig,
-                 last_mode: int, out: torch.Tensor | None = None) -> torch.Tensor:
+                 last_mode: int, out: torch.Tensor | None = None, deferred: bool = False) -> torch.Tensor:
     lib = _lib.lib()
     dims = tuple(vt.shape[-3:])
     d = _lib.dims_arg(dims)
@@ -311,7 +322,8 @@ def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOp
     _lib.check(lib.vr_incstate_init(vt.data_ptr(), grad_m_series[0].data_ptr(), d, float(cfg.dt), u.data_ptr(), st),
                "vr_incstate_init")
     other = torch.empty_like(u)
-    flag = ops.arm()
+    slot = 1 if deferred else 0
+    flag = ops.arm(slot)
     for j in range(cfg.n_t):
         last = j == cfg.n_t - 1
         dst = out if (last and out is not None) else other
@@ -320,7 +332,7 @@ def _incremental(grad_m_series: torch.Tensor, vt: torch.Tensor, ops: TransportOp
             u, other = dst, u
         else:
             u = dst
-    ops.raise_if_flagged("incremental state solve")
+    ops.raise_if_flagged("incremental state solve", slot, deferred)
     return u
 
 

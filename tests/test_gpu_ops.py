@@ -66,6 +66,21 @@ def test_fd8_bit_exact(P, ops_fx):
     assert rel_l2(got, ops_fx["fd8_div"]) < TOL
 
 
+@pytest.mark.parametrize("dims", [(10, 14, 10), (40, 72, 96), (64, 64, 64)])
+def test_fd8_bit_exact_sizes(P, dims):
+    """Ragged tiles, the minimum stencil size and magnitudes from 1e-38 to 1e30
+    (the reciprocal division must reproduce IEEE division bit for bit)."""
+    from oracle import velreg_oracle as O
+    rng = np.random.default_rng(7)
+    g = P.make_grid(dims)
+    scale = 10.0 ** rng.uniform(-38, 30, size=dims)
+    f = (rng.standard_normal(dims) * scale).astype(np.float32)
+    f[rng.random(dims) < 0.05] = 0.0
+    np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), O.grad(f))
+    w = (rng.standard_normal((3,) + dims)).astype(np.float32)
+    np.testing.assert_array_equal(_np(P.fd8_divergence(P.VectorField(g, w)).values), O.div(w))
+
+
 def test_fd8_requires_nine(P):
     g = P.make_grid((8, 16, 16))
     with pytest.raises(P.GridError):

@@ -43,7 +43,10 @@ def main():
     lam = torch.rand((5, n, n, n), device="cuda")
     gm = torch.randn((5, 3, n, n, n), device="cuda")
     l2 = torch.empty(64 * 1024 * 1024, device="cuda")
+    from paper_2209_08189_b200.synth import sphere_template
+    sph = torch.from_numpy(sphere_template(g)[0]).cuda()
     table = {
+        "fd8_grad_sphere": (lambda: P.diffops.fd8_gradient_t(sph, out=out3), N * 16),
         "spec_A": (lambda: ws.apply(_lib.SPEC_A, w, out=out3), 3 * N * 8),
         "spec_inv": (lambda: ws.apply(_lib.SPEC_INVSHIFT, w, out=out3, beta_v=1e-2, shift=1.0), 3 * N * 8),
         "spec_K": (lambda: ws.apply(_lib.SPEC_K, w, out=out3, beta_v=1e-2, beta_w=1e-4), 3 * N * 8),
