@@ -68,6 +68,12 @@ int vr_trace_rk2(const float* v, const int64_t dims[3], double dt, int order, fl
 /* displacement -> absolute points wrapped to [0, 2pi) (Characteristics.points) */
 int vr_disp_to_points(const float* disp, const int64_t dims[3], double* pts, void* stream);
 
+/* Tuning switch (no reference counterpart) for the semi-Lagrangian sweeps:
+ * 1 (default) = shared-memory-staged gathers (stage_tma.cuh; rows of a multiple
+ * of 32 voxels), 0 = direct per-point gathers.  Same results (same taps and
+ * arithmetic order).  Returns the previous mode. */
+int vr_set_gather_mode(int mode);
+
 /* ---- semi-Lagrangian sweeps -------------------------------------------------
  * one step dst = interp(src, X) [* factor]:
  *   state    transport.py:130-133 (factor NULL, forward trace)

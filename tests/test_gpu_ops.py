@@ -198,3 +198,46 @@ def test_ops_vs_oracle(P, n):
     assert rel_l2(_np(P.apply_inv_shifted_A(W, ops, 1.0).data),
                   O.op_inv_shifted(w.astype(np.float64), 1e-2, 1.0)) < TOL
     np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), O.grad(f))
+
+
+@pytest.mark.parametrize("dims,scale", [((256, 256, 256), 0.2), ((32, 32, 32), 1.0), ((16, 20, 32), 0.5),
+                                        ((36, 40, 64), 2.0), ((12, 12, 32), 0.3), ((20, 16, 96), 4.0)])
+def test_staged_gather_matches_direct(P, dims, scale):
+    """The shared-memory-staged sweeps (stage_tma.cuh: per-tile source box copied
+    with cp.async.bulk, taps from shared memory) return the direct per-point
+    gather's floats to the ulp -- smooth fields, large displacements (boxes over
+    budget -> direct fallback inside the same launch) and random displacements
+    -- for the state/adjoint sweep (with factor) and the incremental state
+    step, trilinear and tricubic."""
+    from paper_2209_08189_b200 import _lib, transport
+    from paper_2209_08189_b200.synth import velocity_array
+    g = P.make_grid(dims)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    f = torch.rand(dims, device="cuda", generator=gen)
+    v = P.VectorField(g, scale * velocity_array(2, g))
+    rnd = (torch.rand((3,) + dims, device="cuda", generator=gen) - 0.5) * (2 * min(dims))
+    vt = torch.randn((3,) + dims, device="cuda", generator=gen)
+    gm = torch.randn((3,) + dims, device="cuda", generator=gen)
+    lib = _lib.lib()
+    for order in ("cubic", "linear"):
+        tops = P.TransportOperators(v, P.TransportConfig(4, order))
+        for disp in (tops.forward.displacement, tops.backward.displacement, rnd):
+            outs = {}
+            for mode in (0, 1):
+                prev = lib.vr_set_gather_mode(mode)
+                try:
+                    res = [transport.advect(f, disp, order, factor=tops.adj_factor), transport.advect(f, disp, order)]
+                    b = torch.empty_like(f)
+                    for last in (0, 1, 2):
+                        rc = lib.vr_incstate_step(f.data_ptr(), _lib.dims_arg(dims), disp.data_ptr(), vt.data_ptr(),
+                                                  gm.data_ptr(), 0.25, _lib.ORDER[order], last, b.data_ptr(), None,
+                                                  _lib.stream())
+                        _lib.check(rc, "vr_incstate_step")
+                        res.append(b.clone())
+                    outs[mode] = res
+                finally:
+                    lib.vr_set_gather_mode(prev)
+            torch.cuda.synchronize()
+            for x, y in zip(outs[0], outs[1]):
+                # same taps and arithmetic order; FMA contraction may differ by an ulp
+                assert float((x - y).abs().max()) <= 4e-6 * float(x.abs().max()), (order, dims)
