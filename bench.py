@@ -305,6 +305,14 @@ def run_ours(args):
     e2e_val = max_over_ranks(sum(e2e_times) / len(e2e_times))
 
     # ---- roofline of the dominant kernel -------------------------------------
+    def smem_pipe(ms, pts, pk):
+        if not ms or args.order != "cubic":
+            return None
+        nbytes = 64 * 4 * pts                              # tap bytes delivered to registers per launch
+        peak = 128 * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s: 128 B/clk/SM x 148 SMs
+        ach = nbytes / (ms * 1e-3) / 1e9
+        return {"bytes_per_unit": 256, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
+
     peaks = measured_peaks()
     per_unit = 20.0  # B per interpolated point: 12 B characteristic + 4 B out + 4 B source
     avg_ms, nlaunch = kern.get(dominant, (0.0, 0))
@@ -346,7 +354,10 @@ def run_ours(args):
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
                          "peak_source": peaks["source"], "bytes_per_unit": per_unit,
-                         "units_per_launch": g.num_voxels, "avg_launch_ms": avg_ms},
+                         "units_per_launch": g.num_voxels, "avg_launch_ms": avg_ms,
+                         # the tricubic sweep's binding resource is the shared-memory / L1 data
+                         # pipe (64 taps x 4 B per point through 128 B/clk/SM), not HBM
+                         "smem_pipe": smem_pipe(avg_ms, units, peaks)},
             "kernels": kernels,
             "clocks": clk,
             "cpu_baseline": cpu,
