@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--grid", "--n", dest="n", type=int, default=256)
     ap.add_argument("--order", default="cubic", choices=["cubic", "linear"])
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--beta-w", type=float, default=0.0)

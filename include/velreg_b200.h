@@ -74,6 +74,11 @@ int vr_disp_to_points(const float* disp, const int64_t dims[3], double* pts, voi
  * arithmetic order).  Returns the previous mode. */
 int vr_set_gather_mode(int mode);
 
+/* Tuning switch (no reference counterpart) for the power-of-two spectral path:
+ * 1 (default) = four-step register FFT kernels where they apply (spectral_4step.cuh),
+ * 0 = radix-8 Stockham kernels only.  Returns the previous mode. */
+int vr_set_fft_mode(int mode);
+
 /* ---- semi-Lagrangian sweeps -------------------------------------------------
  * one step dst = interp(src, X) [* factor]:
  *   state    transport.py:130-133 (factor NULL, forward trace)

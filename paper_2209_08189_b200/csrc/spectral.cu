@@ -493,6 +493,11 @@ __global__ void finalize_sum_kernel(const double* __restrict__ partials, int n, 
 }  // namespace vr
 
 #include "spectral_fast.cuh"
+#include "spectral_4step.cuh"
+
+// Four-step register FFT kernels (spectral_4step.cuh) for the line lengths they
+// cover; vr_set_fft_mode(0) selects the Stockham engine for A/B checks.
+static int g_fft_mode = 1;
 
 using namespace vr;
 
@@ -623,6 +628,13 @@ bool needs_f64(int kind) { return kind == VR_SPEC_A || kind == VR_SPEC_A2; }
 
 extern "C" {
 
+int vr_set_fft_mode(int mode) {
+  const int prev = g_fft_mode;
+  g_fft_mode = mode;
+  return prev;
+}
+
+
 int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   if (!out) return VR_ERR_ARG;
   *out = nullptr;
@@ -701,6 +713,14 @@ int vr_spec_plan_destroy(vr_spec_plan* p) {
 
 }  // extern "C"
 
+template <typename F> static void smem_optin(F* f, size_t bytes) {
+  static bool done = false;   // per instantiation
+  if (!done) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done = true;
+  }
+}
+
 // strided c2c pass along x1 (axis 1) or x2 (axis 2) over ncomp spectra
 template <typename C>
 static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, cudaStream_t s) {
@@ -710,6 +730,21 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
   const int64_t es = ax2 ? (int64_t)p->n3h : (int64_t)d.n2 * p->n3h;
   const int n_outer = ax2 ? d.n1 : d.n2;
   const int64_t outer_stride = ax2 ? (int64_t)d.n2 * p->n3h : (int64_t)p->n3h;
+  if (p->fast && g_fft_mode && L == 256) {
+    const int nchunks = (p->n3h + 15) / 16;
+    const size_t sm = sizeof(C) * 16 * fs::line_smem<16>();
+    const double2* twL = ax2 ? p->tw2 : p->tw1;
+    if (inv) {
+      smem_optin(fs::axis256<C, true>, sm);
+      fs::axis256<C, true><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, es, n_outer, outer_stride, p->nspec,
+                                                                          p->n3h, twL);
+    } else {
+      smem_optin(fs::axis256<C, false>, sm);
+      fs::axis256<C, false><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, es, n_outer, outer_stride, p->nspec,
+                                                                           p->n3h, twL);
+    }
+    return;
+  }
   if (p->fast) {
     const double2* tw = ax2 ? p->stw2 : p->stw1;
 #define L_AX(LL)                                                                                      \
@@ -792,6 +827,26 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   const int nc = op.ncomp;
   const double2* Sd = Sext ? reinterpret_cast<const double2*>(Sext) : p->S;
   float2* Tt = Text ? Text : p->T;
+  if (p->fast && g_fft_mode && d.n1 == 256 && nc == 3 && !reduce) {
+    constexpr int LS = 273;
+#define XOP4(XB)                                                                                             \
+  {                                                                                                          \
+    const int nblk = d.n2 * ((p->n3h + XB - 1) / XB);                                                        \
+    if (f64) {                                                                                               \
+      const size_t sm = sizeof(double2) * 3 * XB * LS;                                                       \
+      smem_optin(fs::xop256<double2, XB>, sm);                                                               \
+      fs::xop256<double2, XB><<<nblk, 3 * XB * 16, sm, s>>>(Sd, Tt, d.n2, d.n3, p->n3h, p->tw1, op);         \
+    } else {                                                                                                 \
+      const size_t sm = sizeof(float2) * 3 * XB * LS;                                                        \
+      smem_optin(fs::xop256<float2, XB>, sm);                                                                \
+      fs::xop256<float2, XB><<<nblk, 3 * XB * 16, sm, s>>>(reinterpret_cast<const float2*>(Sd), Tt, d.n2,    \
+                                                           d.n3, p->n3h, p->tw1, op);                        \
+    }                                                                                                        \
+    return nblk;                                                                                             \
+  }
+    XOP4(4)   // 4 kz columns x 3 components per CTA (register-limited to 2 CTAs / SM)
+#undef XOP4
+  }
   if (p->fast) {
     int nblk = 0;
     const float2* S32 = reinterpret_cast<const float2*>(Sd);

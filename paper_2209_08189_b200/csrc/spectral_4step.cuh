@@ -1,0 +1,219 @@
+// Four-step register FFTs for the power-of-two fast path (L = 16 x R2, R2 in {8, 16}).
+//
+// The Stockham engine (spectral_fast.cuh) round-trips every radix-8 stage
+// through shared memory: ~8 shared accesses per element per line FFT, and the
+// passes measured 92-97 % of the L1/shared data pipe (profiles/r1_ncu_spectral_fast.txt).
+// Here a line of L = 16 * R2 elements is held by R2 threads:
+//   thread t owns x[t + R2 m], m = 0..15        (strided, coalesced across lines)
+//   1. DFT-16 over m in registers                -> y_t[k1]
+//   2. twiddle y_t[k1] *= W_L^{t k1}             (from the plan's W_L table)
+//   3. one shared-memory transpose (row t, column k1; rows padded to 17)
+//   4. DFT-R2 over t for each k1 the thread owns -> X[k1 + 16 k2]
+// so a line FFT costs one shared write + one shared read per element.  Lines
+// of a CTA are interleaved so that consecutive lanes are consecutive lines:
+// every global load / store of a warp is a contiguous run along the line index.
+// Inverse = conjugate twiddles (unnormalised, like the Stockham engine).
+#pragma once
+
+namespace vr {
+namespace fs {
+
+// W_16^m constants (forward sign), m = 0..15
+__device__ __forceinline__ double w16c(int m) {
+  constexpr double c[16] = {1.0, 0.92387953251128673848, 0.70710678118654752440, 0.38268343236508977173,
+                            0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128673848,
+                            -1.0, -0.92387953251128673848, -0.70710678118654752440, -0.38268343236508977173,
+                            0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128673848};
+  return c[m & 15];
+}
+__device__ __forceinline__ double w16s(int m) { return -w16c((m + 12) & 15); }   // -sin(2 pi m / 16)
+
+template <typename C>
+__device__ __forceinline__ C w16(int m, bool inv) {
+  C w;
+  w.x = (decltype(w.x))w16c(m);
+  const double s = w16s(m);
+  w.y = (decltype(w.y))(inv ? -s : s);
+  return w;
+}
+
+// in-place DFT-16, natural order in and out
+template <typename C>
+__device__ __forceinline__ void dft16(C (&v)[16], bool inv) {
+  // n = 4 n1 + n2, k = k1 + 4 k2
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2], inv);   // v[4 k1 + n2]
+#pragma unroll
+  for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2) {
+      const int m = k1 * n2;
+      C& a = v[4 * k1 + n2];
+      if (m == 4) a = rot(a, inv);   // W16^4 = -i
+      else a = cmul(a, w16<C>(m, inv));
+    }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3], inv);   // v[4 k1 + k2]
+  C o[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) o[k1 + 4 * k2] = v[4 * k1 + k2];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+
+// in-place DFT-8, natural order
+template <typename C>
+__device__ __forceinline__ void dft8(C (&v)[8], bool inv) {
+  C e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  C o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4(e0, e1, e2, e3, inv);
+  dft4(o0, o1, o2, o3, inv);
+  o1 = cmul(o1, w16<C>(2, inv));
+  o2 = rot(o2, inv);
+  o3 = cmul(o3, w16<C>(6, inv));
+  v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
+}
+
+template <int R2> __host__ __device__ constexpr int line_smem() { return R2 * 17 + 1; }   // elements, odd
+
+// Steps 1-4 for one line held by R2 threads (thread t, 16 values x[t + R2 m] in v).
+// `sm` = this line's shared scratch (line_smem<R2>() elements); `tw` = W_L table
+// (L = 16 R2 entries, forward sign).  The CTA must __syncthreads() between calls
+// that reuse `sm` (the caller owns the barrier because lines span warps).
+// On return the thread owns X[k1 + 16 k2] for its k1 set:
+//   R2 = 16: k1 = t, k2 = 0..15 -> v[k2]
+//   R2 =  8: k1 = t and t + 8, k2 = 0..7 -> v[k2] (k1 = t), v[8 + k2] (k1 = t + 8)
+template <typename C, int R2>
+__device__ __forceinline__ void line_fft(C (&v)[16], int t, C* sm, const double2* __restrict__ tw, bool inv) {
+  constexpr int L = 16 * R2;
+  dft16(v, inv);
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    double2 w = __ldg(tw + ((t * k1) & (L - 1)));
+    if (inv) w.y = -w.y;
+    v[k1] = cmul(v[k1], cvt<C>(w));
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) sm[t * 17 + k1] = v[k1];
+  __syncthreads();
+  if constexpr (R2 == 16) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = sm[s * 17 + t];
+    dft16(v, inv);
+  } else {
+    C a[8], b[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      a[s] = sm[s * 17 + t];
+      b[s] = sm[s * 17 + t + 8];
+    }
+    dft8(a, inv);
+    dft8(b, inv);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      v[s] = a[s];
+      v[8 + s] = b[s];
+    }
+  }
+}
+
+// output frequency of v[u] for thread t (see line_fft)
+template <int R2>
+__device__ __forceinline__ int out_freq(int t, int u) {
+  if constexpr (R2 == 16) return t + 16 * u;
+  else return (u < 8) ? t + 16 * u : t + 8 + 16 * (u - 8);
+}
+
+// ---- strided axis pass (x2 or plain x1), L = 256: NB lines (consecutive kz) per CTA,
+// 16 threads per line, lane = line + NB * t.  grid (n_outer * nchunks, ncomp)
+template <typename C, bool INV>
+__global__ void __launch_bounds__(256, 2) axis256(C* __restrict__ S, int64_t es, int n_outer, int64_t outer_stride,
+                                               int64_t comp_stride, int n3h, const double2* __restrict__ tw) {
+  constexpr int R2 = 16, NB = 16;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  C* smem = reinterpret_cast<C*>(fs_smem);
+  const int q = threadIdx.x % NB, t = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int o = blockIdx.x / nchunks, kz0 = (blockIdx.x - o * nchunks) * NB;
+  const bool ok = kz0 + q < n3h;
+  C* base = S + blockIdx.y * comp_stride + o * outer_stride + kz0 + q;
+  C v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (ok) v[m] = base[(int64_t)(t + R2 * m) * es];
+    else { v[m].x = 0; v[m].y = 0; }
+  }
+  line_fft<C, R2>(v, t, smem + q * line_smem<R2>(), tw, INV);
+  if (ok) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) base[(int64_t)out_freq<R2>(t, u) * es] = v[u];
+  }
+}
+
+// ---- X pass for 3-component operators, L = n1 = 256: forward (CF) -> symbol (f64)
+// -> inverse (f32) -> T.  One CTA = fixed x2 row j, XB consecutive kz, all 3
+// components: 3 * XB lines of 16 threads, lane = q + XB * (t + 16 c).
+// The forward spectrum goes through one shared tile (per line, natural
+// frequency order) so the symbol sees the 3 components of a wavenumber
+// together (the Leray / K blend couples them); the inverse runs in f32 (its
+// rounding is relative to the output, like the x2 / x3 inverse passes).
+template <typename CF, int XB>
+__global__ void __launch_bounds__(3 * XB * 16, 8 / XB) xop256(const CF* __restrict__ S, float2* __restrict__ T, int n2,
+                                                              int n3, int n3h, const double2* __restrict__ tw,
+                                                              SpecOp op) {
+  constexpr int R2 = 16, L = 256, LS = line_smem<R2>() > L ? line_smem<R2>() : L;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  CF* tile = reinterpret_cast<CF*>(fs_smem);             // [c][q] lines of LS elements
+  const int q = threadIdx.x % XB, t = (threadIdx.x / XB) % 16, c = threadIdx.x / (16 * XB);
+  const int nchunks = (n3h + XB - 1) / XB;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * XB;
+  const bool ok = kz0 + q < n3h;
+  const int64_t lstride = (int64_t)n2 * n3h;
+  const CF* sb = S + (int64_t)j * n3h + kz0 + q;
+  CF* line = tile + (c * XB + q) * LS;
+  CF v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (ok) v[m] = sb[op.xoff(c, t + R2 * m, lstride)];
+    else { v[m].x = 0; v[m].y = 0; }
+  }
+  line_fft<CF, R2>(v, t, line, tw, false);
+  __syncthreads();   // every line finished reading its transpose scratch
+#pragma unroll
+  for (int u = 0; u < 16; ++u) line[out_freq<R2>(t, u)] = v[u];
+  __syncthreads();
+  // symbol at (k1 = freq along x1, k2 = row j, k3 = kz) for the 3 components
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g);
+  for (int e = threadIdx.x; e < XB * L; e += blockDim.x) {
+    const int qq = e / L, m = e - qq * L;
+    double2 vals[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) vals[cc] = to_d(tile[(cc * XB + qq) * LS + m]);
+    apply_symbol(op, (double)signed_freq(m, L), k2, (double)(kz0 + qq), vals);
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) tile[(cc * XB + qq) * LS + m] = cvt<CF>(vals[cc]);
+  }
+  __syncthreads();
+  float2 w[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const CF a = line[t + R2 * m];
+    w[m] = make_float2((float)a.x, (float)a.y);
+  }
+  __syncthreads();   // the tile is reused as f32 transpose scratch
+  float2* fline = reinterpret_cast<float2*>(fs_smem) + (c * XB + q) * LS;
+  line_fft<float2, R2>(w, t, fline, tw, true);
+  if (ok) {
+    float2* tb = T + (int64_t)j * n3h + kz0 + q;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tb[op.xoff(c, out_freq<R2>(t, u), lstride)] = w[u];
+  }
+}
+
+}  // namespace fs
+}  // namespace vr
