@@ -27,8 +27,16 @@ namespace vr {
 namespace stg {
 
 constexpr int NT = 128;                 // threads per CTA
-constexpr int PPT = 4;                  // points per thread
-constexpr int kSmemBudget = 36 * 1024;  // bytes of staged box per CTA (6 CTAs / SM)
+
+// Tile / residency configuration: PPT points per thread (tile = PPT * NT
+// points), box budget per CTA, CTAs per SM the launch bounds aim for.  (PPT = 2
+// with 24 KB boxes and 9 CTAs / SM measured 6 % slower: the halo share of the
+// box grows faster than residency helps.)
+template <int PPT_> struct Cfg {
+  static constexpr int PPT = PPT_;
+  static constexpr int kSmemBudget = 36 * 1024;
+  static constexpr int kCtas = 6;
+};
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -58,9 +66,9 @@ __device__ __forceinline__ int floor4(int a) { return a & ~3; }   // floor to a 
 struct Tile {
   int tk, tj;
 };
-inline Tile tile_for(const Dims& d) {
+inline Tile tile_for(const Dims& d, int ppt) {
   const int tk = d.n3 >= NT ? NT : d.n3;
-  return Tile{tk, PPT * (NT / tk)};
+  return Tile{tk, ppt * (NT / tk)};
 }
 inline bool staged_ok(const Dims& d) { return d.n3 % 32 == 0 && d.n2 >= 4; }
 
@@ -104,9 +112,11 @@ struct PointSplit {
 // shared-memory latency.)  A box over budget, or a tile with a non-finite or
 // huge displacement, gathers directly.  ORDER: ORDER_CUBIC or ORDER_LINEAR;
 // epi(idx, v) writes voxel idx.
-template <int ORDER, bool SLAB, class Epi>
-__global__ void __launch_bounds__(NT, 6) sweep_kernel(PlaneSrc<1, SLAB> src, Dims d, const float* __restrict__ disp,
-                                                      Tile T, int x0, Epi epi) {
+template <int ORDER, bool SLAB, class Epi, int PPT>
+__global__ void __launch_bounds__(NT, Cfg<PPT>::kCtas) sweep_kernel(PlaneSrc<1, SLAB> src, Dims d,
+                                                                    const float* __restrict__ disp, Tile T, int x0,
+                                                                    Epi epi) {
+  constexpr int kSmemBudget = Cfg<PPT>::kSmemBudget;
   constexpr int LO = ORDER == ORDER_CUBIC ? 1 : 0;   // stencil reach below / above the base index
   constexpr int HI = ORDER == ORDER_CUBIC ? 2 : 1;
   extern __shared__ __align__(128) float box[];

@@ -386,9 +386,9 @@ static bool use_staged(int order, const Dims& d) {
 template <int ORD, bool SLAB, class Epi>
 static void launch_staged(const PlaneSrc<1, SLAB>& ps, const Dims& d, const float* disp, int x0, int nx, Epi epi,
                           cudaStream_t s) {
-  const stg::Tile T = stg::tile_for(d);
-  stg::sweep_kernel<ORD, SLAB, Epi><<<stg::sweep_grid(d, T, nx), stg::NT, stg::kSmemBudget, s>>>(ps, d, disp, T, x0,
-                                                                                                 epi);
+  const stg::Tile T = stg::tile_for(d, 4);
+  stg::sweep_kernel<ORD, SLAB, Epi, 4><<<stg::sweep_grid(d, T, nx), stg::NT, stg::Cfg<4>::kSmemBudget, s>>>(
+      ps, d, disp, T, x0, epi);
 }
 
 static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], const float* disp, const float* factor,
