@@ -102,6 +102,14 @@ int vr_incstate_step(const float* u, const int64_t dims[3], const float* disp_fw
 int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, const int64_t dims[3], double dt,
                   float* out, void* stream);
 
+/* Lean layout (no stored grad-m series): one term j of the same trapezoid,
+ * weight w_j = dt/2 at the ends and dt inside, with an f64 accumulator acc
+ * (3 x N doubles).  mode 0 = first term (acc = term), 1 = middle (acc +=),
+ * 2 = last (acc += term, out = (float)acc).  Calling it for j = 0..n_t in order
+ * reproduces vr_body_force bit for bit (optim.py:162-171 accumulates in f64). */
+int vr_body_force_term(const float* lam, const float* gradm, const int64_t dims[3], double weight, int mode,
+                       double* acc, float* out, void* stream);
+
 /* label transport step (synth.py:121-131): source = labels_in==label_id
  * (if labels_in) else src; destination = float field (dst) or thresholded
  * write of label_id where value >= 0.5 (labels_out). */

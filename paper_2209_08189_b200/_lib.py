@@ -40,6 +40,7 @@ _SIGS = {
     "vr_incstate_init": [_p, _p, _dims_t, _f64, _p, _p],
     "vr_incstate_step": [_p, _dims_t, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],
     "vr_body_force": [_p, _p, _i32, _dims_t, _f64, _p, _p],
+    "vr_body_force_term": [_p, _p, _dims_t, _f64, _i32, _p, _p, _p],
     "vr_label_step": [_p, _p, _i32, _dims_t, _p, _i32, _p, _p, _p],
     "vr_fd8_grad": [_p, _dims_t, _p, _p],
     "vr_fd8_div": [_p, _dims_t, _p, _p],

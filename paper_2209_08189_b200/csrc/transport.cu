@@ -238,6 +238,39 @@ __global__ void __launch_bounds__(256) body_force_kernel(const float* __restrict
   out[2 * N + idx] = (float)a2;
 }
 
+// One trapezoid term of the body force with the f64 accumulator kept in HBM
+// (lean layout: grad m^j recomputed per term instead of stored as a series).
+// The per-voxel arithmetic and summation order are body_force_kernel's, so the
+// result is bit-identical:  acc (+)= (double)(RN(w*(double)lam) * g);  on the
+// last term out = (float)acc.  mode: 0 = first term (acc =), 1 = middle,
+// 2 = last (acc += then write out).
+__global__ void __launch_bounds__(256) body_force_term_kernel(const float* __restrict__ lam,
+                                                              const float* __restrict__ g, int64_t N, double w,
+                                                              int mode, double* __restrict__ acc,
+                                                              float* __restrict__ out) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  const float wl = (float)(w * (double)__ldg(lam + idx));
+  double a0 = (double)(wl * __ldg(g + idx));
+  double a1 = (double)(wl * __ldg(g + N + idx));
+  double a2 = (double)(wl * __ldg(g + 2 * N + idx));
+  const double z0 = mode != 0 ? acc[idx] : 0.0;          // 0.0 + x keeps body_force_kernel's zero signs
+  const double z1 = mode != 0 ? acc[N + idx] : 0.0;
+  const double z2 = mode != 0 ? acc[2 * N + idx] : 0.0;
+  a0 = z0 + a0;
+  a1 = z1 + a1;
+  a2 = z2 + a2;
+  if (mode == 2) {
+    out[idx] = (float)a0;
+    out[N + idx] = (float)a1;
+    out[2 * N + idx] = (float)a2;
+  } else {
+    acc[idx] = a0;
+    acc[N + idx] = a1;
+    acc[2 * N + idx] = a2;
+  }
+}
+
 // ---- label transport (synth.py:121-131) ---------------------------------------
 // First step gathers the indicator of `id` straight from the label map; the last
 // step thresholds at 0.5 and writes `id` (labels processed in ascending order, so
@@ -542,6 +575,18 @@ int vr_body_force(const float* lam_series, const float* gradm_series, int n_t, c
   if (!lam_series || !gradm_series || !out || n_t < 1) return VR_ERR_ARG;
   body_force_kernel<<<grid_for(d.n(), 256), 256, 0, (cudaStream_t)stream>>>(lam_series, gradm_series, n_t, d.n(),
                                                                             dt, out);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_body_force_term(const float* lam, const float* gradm, const int64_t dims[3], double weight, int mode,
+                       double* acc, float* out, void* stream) {
+  Dims d;
+  int rc = dims_from(dims, &d);
+  if (rc) return rc;
+  if (!lam || !gradm || !acc || mode < 0 || mode > 2 || (mode == 2 && !out)) return VR_ERR_ARG;
+  body_force_term_kernel<<<grid_for(d.n(), 256), 256, 0, (cudaStream_t)stream>>>(lam, gradm, d.n(), weight, mode,
+                                                                                 acc, out);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }

@@ -19,3 +19,27 @@ def set_reproducible(flag: bool) -> None:
 
 def reproducible() -> bool:
     return _reproducible
+
+
+# Memory layout of the grad-m series (optim.py:127-135 keeps (n_t+1) x 3 fields).
+# "auto": store it unless it would take more than a third of the free device
+# memory, otherwise recompute grad m^j per use (transport.LazyGradientSeries;
+# results are bit-identical, FD8 is deterministic).  "stored" / "lean" force one.
+_grad_layout = "auto"
+
+
+def set_grad_layout(mode: str) -> None:
+    global _grad_layout
+    if mode not in ("auto", "stored", "lean"):
+        raise ValueError(f"unknown grad-m layout {mode!r}")
+    _grad_layout = mode
+
+
+def lean_layout(series_bytes: int, device) -> bool:
+    if _grad_layout != "auto":
+        return _grad_layout == "lean"
+    import torch
+    if device.type != "cuda":
+        return False
+    free, _ = torch.cuda.mem_get_info(device)
+    return series_bytes > free // 3

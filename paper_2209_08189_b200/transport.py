@@ -303,6 +303,24 @@ def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: Transport
     ops.raise_if_flagged("adjoint solve", slot, deferred)
 
 
+class LazyGradientSeries:
+    """grad m^j computed on demand (lean layout): indexing returns the FD8
+    gradient of snapshot j in a reused (3,) + dims buffer, valid until the next
+    index on the same stream (kernels consuming it are stream-ordered before
+    the next FD8 launch overwrites it).  Saves (n_t+1) * 12 B/voxel of HBM --
+    what makes C3 (1024^3, n_t = 16) fit on 4 B200s."""
+
+    def __init__(self, m_series: torch.Tensor):
+        self.m_series = m_series
+        self.buf = torch.empty((3,) + tuple(m_series.shape[1:]), dtype=torch.float32, device=m_series.device)
+
+    def __len__(self):
+        return self.m_series.shape[0]
+
+    def __getitem__(self, j: int) -> torch.Tensor:
+        return fd8_gradient_t(self.m_series[j], out=self.buf)
+
+
 def gradient_series(m_series: torch.Tensor) -> torch.Tensor:
     """FD8 gradient of every snapshot, (n_t+1, 3) + dims (optim.py:127-135)."""
     out = torch.empty((m_series.shape[0], 3) + tuple(m_series.shape[1:]), dtype=torch.float32,

@@ -52,3 +52,22 @@ def test_error_hierarchy():
         assert issubclass(e, P.VelregError)
     from paper_2209_08189_b200._lib import NativeError
     assert issubclass(NativeError, P.VelregError)
+
+
+def test_grad_layout_switch():
+    """runtime.set_grad_layout validates its argument; forced modes bypass the
+    free-memory heuristic (which keeps the stored series on CPU tensors)."""
+    import pytest
+    import torch
+    from paper_2209_08189_b200 import runtime
+    with pytest.raises(ValueError):
+        runtime.set_grad_layout("bogus")
+    try:
+        runtime.set_grad_layout("lean")
+        assert runtime.lean_layout(1, torch.device("cpu"))
+        runtime.set_grad_layout("stored")
+        assert not runtime.lean_layout(1 << 60, torch.device("cpu"))
+        runtime.set_grad_layout("auto")
+        assert not runtime.lean_layout(1 << 60, torch.device("cpu"))
+    finally:
+        runtime.set_grad_layout("auto")
