@@ -22,10 +22,12 @@ def reproducible() -> bool:
 
 
 # Memory layout of the grad-m series (optim.py:127-135 keeps (n_t+1) x 3 fields).
-# "auto": store it unless it would take more than a third of the free device
-# memory, otherwise recompute grad m^j per use (transport.LazyGradientSeries;
+# "auto": store it unless it would take more than a third of the device memory
+# not yet allocated by torch, otherwise recompute grad m^j per use (transport.LazyGradientSeries;
 # results are bit-identical, FD8 is deterministic).  "stored" / "lean" force one.
-_grad_layout = "auto"
+import os as _os
+
+_grad_layout = _os.environ.get("VR_GRAD_LAYOUT", "auto")
 
 
 def set_grad_layout(mode: str) -> None:
@@ -41,5 +43,8 @@ def lean_layout(series_bytes: int, device) -> bool:
     import torch
     if device.type != "cuda":
         return False
-    free, _ = torch.cuda.mem_get_info(device)
+    # allocator statistics, not cudaMemGetInfo (a driver round trip that costs
+    # ~4 ms per call on B200 -- measured as idle gaps in tools/timeline.py)
+    total = torch.cuda.get_device_properties(device).total_memory
+    free = total - torch.cuda.memory_allocated(device)
     return series_bytes > free // 3
