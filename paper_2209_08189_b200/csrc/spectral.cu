@@ -964,36 +964,24 @@ int vr_spec_plan_dims(const vr_spec_plan* p, int64_t dims_out[3]) {
 // ---------------------------------------------------------------------------------
 namespace vr {
 
-template <typename C>
-__global__ void pack_kernel(const C* __restrict__ S, C* __restrict__ out, int ncomp, int L1, int N2, int n3h, int P) {
+// Rank-blocked transpose layout [q][c][i][jl][kz] <-> slab layout [c][i][j][kz]
+// (j = q * L2 + jl).  One warp moves one contiguous kz row: a single 32-bit
+// index decomposition per row instead of 64-bit divisions per element.
+template <typename C, bool PACK>
+__global__ void __launch_bounds__(256) rowmove_kernel(const C* __restrict__ src, C* __restrict__ dst, int ncomp,
+                                                      int L1, int N2, int n3h, int P) {
   const int L2 = N2 / P;
-  const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    // out layout [q][c][i][jl][kz]: one contiguous block per destination rank
-    int64_t r = e;
-    const int kz = (int)(r % n3h); r /= n3h;
-    const int jl = (int)(r % L2); r /= L2;
-    const int i = (int)(r % L1); r /= L1;
-    const int c = (int)(r % ncomp);
-    const int q = (int)(r / ncomp);
-    out[e] = S[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz];
-  }
-}
-
-__global__ void unpack_kernel(const float2* __restrict__ in, float2* __restrict__ T, int ncomp, int L1, int N2, int n3h,
-                              int P) {
-  const int L2 = N2 / P;
-  const int64_t total = (int64_t)ncomp * L1 * N2 * n3h;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    // in layout [q][c][i][jl][kz]
-    int64_t r = e;
-    const int kz = (int)(r % n3h); r /= n3h;
-    const int jl = (int)(r % L2); r /= L2;
-    const int i = (int)(r % L1); r /= L1;
-    const int c = (int)(r % ncomp);
-    const int q = (int)(r / ncomp);
-    T[(((int64_t)c * L1 + i) * N2 + q * L2 + jl) * n3h + kz] = in[e];
-  }
+  const int rows = ncomp * L1 * N2;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int j = row % N2, ci = row / N2;   // slab row (c, i, j)
+  const int i = ci % L1, c = ci / L1;
+  const int q = j / L2, jl = j - q * L2;
+  const int64_t slab = (int64_t)row * n3h;
+  const int64_t blk = ((((int64_t)q * ncomp + c) * L1 + i) * L2 + jl) * n3h;
+  const C* a = src + (PACK ? slab : blk);
+  C* b = dst + (PACK ? blk : slab);
+  for (int kz = lane; kz < n3h; kz += 32) b[kz] = a[kz];
 }
 
 }  // namespace vr
@@ -1009,13 +997,15 @@ int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int 
   int rc = spec_forward(pl, in, ncomp, s, f64 != 0);
   if (rc) return rc;
   const int64_t n = pl->nspec * ncomp;
+  const unsigned g = (unsigned)((ncomp * pl->d.n1 * pl->d.n2 + 7) / 8);
+  (void)n;
   if (f64)
-    pack_kernel<double2><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(pl->S, reinterpret_cast<double2*>(sendbuf), ncomp,
-                                                                   pl->d.n1, pl->d.n2, pl->n3h, nranks);
+    rowmove_kernel<double2, true><<<g, 256, 0, s>>>(pl->S, reinterpret_cast<double2*>(sendbuf), ncomp, pl->d.n1,
+                                                    pl->d.n2, pl->n3h, nranks);
   else
-    pack_kernel<float2><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(reinterpret_cast<const float2*>(pl->S),
-                                                                  reinterpret_cast<float2*>(sendbuf), ncomp, pl->d.n1,
-                                                                  pl->d.n2, pl->n3h, nranks);
+    rowmove_kernel<float2, true><<<g, 256, 0, s>>>(reinterpret_cast<const float2*>(pl->S),
+                                                   reinterpret_cast<float2*>(sendbuf), ncomp, pl->d.n1, pl->d.n2,
+                                                   pl->n3h, nranks);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
@@ -1056,8 +1046,9 @@ int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nran
   if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = pl->nspec * ncomp;
-  unpack_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(reinterpret_cast<const float2*>(recv_inv), pl->T, ncomp,
-                                                           pl->d.n1, pl->d.n2, pl->n3h, nranks);
+  (void)n;
+  rowmove_kernel<float2, false><<<(unsigned)((ncomp * pl->d.n1 * pl->d.n2 + 7) / 8), 256, 0, s>>>(
+      reinterpret_cast<const float2*>(recv_inv), pl->T, ncomp, pl->d.n1, pl->d.n2, pl->n3h, nranks);
   spec_inverse_yz(pl, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
   return VR_OK;
