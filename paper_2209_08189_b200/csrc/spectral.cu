@@ -827,6 +827,18 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   const int nc = op.ncomp;
   const double2* Sd = Sext ? reinterpret_cast<const double2*>(Sext) : p->S;
   float2* Tt = Text ? Text : p->T;
+  if (p->fast && nc == 3 && !reduce && xb(d.n1, 3) == 0) {
+    // x1 lines of 2048: no 3-component tile fits; component-diagonal symbols run
+    // one component at a time (the coupled K symbol is rejected by the callers)
+    SpecOp o1 = op;
+    o1.ncomp = 1;
+    const int64_t cstride = (int64_t)d.n1 * d.n2 * p->n3h;   // single-domain layout [c][i][j][kz]
+    const size_t esz = f64 ? sizeof(double2) : sizeof(float2);
+    int nblk = 0;
+    for (int c = 0; c < 3; ++c)
+      nblk = spec_xpass(p, o1, false, s, f64, reinterpret_cast<const char*>(Sd) + c * cstride * esz, Tt + c * cstride);
+    return nblk;
+  }
   if (p->fast && g_fft_mode && d.n1 == 256 && nc == 3 && !reduce) {
     constexpr int LS = 273;
 #define XOP4(XB)                                                                                             \
@@ -894,6 +906,7 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
                   double shift, double sigma, double alpha, const float* add, float* out, void* stream) {
   if (!p || !in || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
+  if (kind == VR_SPEC_K && p->fast && xb(p->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
   const bool f64 = needs_f64(kind);
@@ -1019,6 +1032,7 @@ int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v
   if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3) || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
   if (!px->fast) return VR_ERR_UNSUPPORTED;
+  if (ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048: 3-component tiles do not fit
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
   spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, reinterpret_cast<float2*>(xout));
   VR_CHECK_LAUNCH();

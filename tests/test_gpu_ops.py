@@ -242,3 +242,23 @@ def test_staged_gather_matches_direct(P, dims, scale):
                 for x, y in zip(outs[0], outs[mode]):
                     # same taps and arithmetic order; FMA contraction may differ by an ulp
                     assert float((x - y).abs().max()) <= 4e-6 * float(x.abs().max()), (order, dims, mode)
+
+
+@pytest.mark.parametrize("dims", [(2048, 8, 16), (1024, 16, 16), (256, 256, 32)])
+def test_spectral_long_x1_lines(P, dims):
+    """Power-of-two x1 lines up to 2048 (the transposed x1 pass of an 8-rank
+    weak-scaling run has N1 = 2048): A and the shifted inverse against the
+    oracle; the coupled K at N1 = 2048 is rejected loudly, not mis-computed."""
+    from oracle import velreg_oracle as O
+    g = P.make_grid(dims)
+    w = np.random.default_rng(7).standard_normal((3,) + dims).astype(np.float32)
+    ops = P.RegOperators.for_grid(g, 1e-2, 1e-4)
+    W = P.VectorField(g, w)
+    assert rel_l2(_np(P.apply_A(W, ops).data), O.op_A(w.astype(np.float64))) < TOL
+    assert rel_l2(_np(P.apply_inv_shifted_A(W, ops, 1.0).data),
+                  O.op_inv_shifted(w.astype(np.float64), 1e-2, 1.0)) < TOL
+    if dims[0] >= 2048:
+        with pytest.raises(Exception):
+            P.apply_K(W, ops)
+    else:
+        assert rel_l2(_np(P.apply_K(W, ops).data), O.op_K(w.astype(np.float64), 1e-2, 1e-4)) < TOL
