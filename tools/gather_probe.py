@@ -40,6 +40,11 @@ def main():
         "advect_fac": (lambda: transport.advect(f, tops.backward.displacement, "cubic", factor=tops.adj_factor,
                                                 out=out), 24 * N),
         "advect_lin": (lambda: transport.advect(f, topl.forward.displacement, "linear", out=out), 20 * N),
+        "advect_lin_fac": (lambda: transport.advect(f, topl.backward.displacement, "linear", factor=topl.adj_factor,
+                                                    out=out), 24 * N),
+        "incstep_lin": (lambda: lib.vr_incstate_step(f.data_ptr(), _lib.dims_arg(dims),
+                                                     topl.forward.displacement.data_ptr(), vt.data_ptr(), gm.data_ptr(),
+                                                     0.25, 1, 0, out.data_ptr(), None, _lib.stream()), 44 * N),
         "incstep": (lambda: lib.vr_incstate_step(f.data_ptr(), _lib.dims_arg(dims),
                                                  tops.forward.displacement.data_ptr(), vt.data_ptr(), gm.data_ptr(),
                                                  0.25, 3, 0, out.data_ptr(), None, _lib.stream()), 44 * N),
