@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256, 2) axis256(C* __restrict__ S, int64_t es,
 // together (the Leray / K blend couples them); the inverse runs in f32 (its
 // rounding is relative to the output, like the x2 / x3 inverse passes).
 template <typename CF, int XB>
-__global__ void __launch_bounds__(3 * XB * 16, 12 / XB) xop256(const CF* __restrict__ S, float2* __restrict__ T, int n2,
+__global__ void __launch_bounds__(3 * XB * 16, (sizeof(CF) == 8 ? 20 : 12) / XB) xop256(const CF* __restrict__ S, float2* __restrict__ T, int n2,
                                                               int n3, int n3h, const double2* __restrict__ tw,
                                                               SpecOp op) {
   constexpr int R2 = 16, L = 256, LS = line_smem<R2>() > L ? line_smem<R2>() : L;
