@@ -132,7 +132,7 @@ __device__ __forceinline__ int out_freq(int t, int u) {
 // ---- strided axis pass (x2 or plain x1), L = 256: NB lines (consecutive kz) per CTA,
 // 16 threads per line, lane = line + NB * t.  grid (n_outer * nchunks, ncomp)
 template <typename C, bool INV>
-__global__ void __launch_bounds__(256, 2) axis256(C* __restrict__ S, int64_t es, int n_outer, int64_t outer_stride,
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256(C* __restrict__ S, int64_t es, int n_outer, int64_t outer_stride,
                                                int64_t comp_stride, int n3h, const double2* __restrict__ tw) {
   constexpr int R2 = 16, NB = 16;
   extern __shared__ __align__(16) unsigned char fs_smem[];
