@@ -138,3 +138,43 @@ def c2_problem(grid: Grid, order: str = "cubic", n_t: int = 4):
     m1 = solve_state(m0, vtrue, cfg, tops)
     lab1 = transport_labels(lab0, vtrue, cfg, tops)
     return m0, m1, lab0, lab1, vtrue
+
+
+def _device_axes(grid: Grid):
+    """Broadcastable f64 lattice coordinates on the device: (N1,1,1), (1,N2,1), (1,1,N3)."""
+    dev = _lib.device()
+    ax = [torch.arange(n, dtype=torch.float64, device=dev) * (2 * math.pi / n) for n in grid.dims]
+    return ax[0].view(-1, 1, 1), ax[1].view(1, -1, 1), ax[2].view(1, 1, -1)
+
+
+def c2_problem_device(grid: Grid, order: str = "cubic", n_t: int = 4):
+    """c2_problem with the inputs evaluated on the device in f64 (same formulas
+    as sphere_template / velocity_array, no host volume): for 1024^3 and up,
+    where the host-side f64 lattice alone would take ~26 GB per array."""
+    x, y, z = _device_axes(grid)
+    r = torch.sqrt((x - math.pi) ** 2 + (y - math.pi) ** 2 + (z - math.pi) ** 2)
+    m0 = ScalarField(grid, (0.5 * (1.0 - torch.tanh((r - 1.2) / 0.19635))).to(torch.float32))
+    lab0 = LabelMap(grid, (r <= 1.2).to(torch.int32))
+    del r
+    xc, yc, zc = x - math.pi, y - math.pi, z - math.pi
+    comps = []
+    for c in range(3):
+        acc = torch.zeros(grid.dims, dtype=torch.float64, device=x.device)
+        for k in range(1, 3):
+            a = k ** -0.5
+            if c == 0:
+                acc += a * torch.cos(k * yc) * torch.cos(k * xc)
+            elif c == 1:
+                acc += a * torch.sin(k * zc) * torch.sin(k * yc)
+            else:
+                acc += a * torch.cos(k * xc) * torch.cos(k * zc)
+        comps.append((0.2 * acc).to(torch.float32))
+        del acc
+    vtrue = VectorField(grid, torch.stack(comps))
+    del comps
+    cfg = TransportConfig(n_t, order)
+    tops = TransportOperators(vtrue, cfg)
+    m1 = solve_state(m0, vtrue, cfg, tops)
+    lab1 = transport_labels(lab0, vtrue, cfg, tops)
+    del tops
+    return m0, m1, lab0, lab1, vtrue

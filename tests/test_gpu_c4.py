@@ -1,0 +1,44 @@
+"""C4: the 256^3 level of the 1024^3 downsampling study
+against the LIVE reference run on the same inputs (tests/golden/c4_256.json,
+tests/golden/make_golden_c4.py).  The device regenerates the 1024^3 pair,
+restricts by 4 and must reproduce the reference's input checksum before the
+registration is compared (north-star bars: 1e-3 on residual / J, PCG counts
+and termination identical, +-0.5 pp Dice).  Needs ~75 GB of HBM.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_json
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-3
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c4_256.json")), reason="fixture not generated")
+def test_c4_level4_matches_reference():
+    import torch
+    import paper_2209_08189_b200 as P
+    from paper_2209_08189_b200.synth import c2_problem_device
+    gold = golden_json("c4_256.json")
+    g = P.make_grid((1024,) * 3)
+    m0, m1, l0, l1, vt = c2_problem_device(g, "linear", 16)
+    del vt
+    m0c, m1c, l0c, l1c = (P.restrict(f, 4) for f in (m0, m1, l0, l1))
+    del m0, m1, l0, l1
+    torch.cuda.empty_cache()
+    assert hashlib.sha256(m1c.numpy().tobytes()).hexdigest() == gold["m1_sha256"]
+    assert hashlib.sha256(l1c.numpy().tobytes()).hexdigest() == gold["labels1_sha256"]
+    cfg = P.RegistrationConfig(**gold["config"])
+    v, diag = P.gauss_newton_register(m0c, m1c, cfg)
+    rec = diag.iterations
+    assert [r.pcg_iterations for r in rec] == gold["pcg"]
+    np.testing.assert_allclose([r.objective for r in rec], gold["objective"], rtol=RTOL)
+    assert abs(diag.relative_residual / gold["relative_residual"] - 1) < RTOL
+    assert abs(diag.j_min / gold["j_min"] - 1) < RTOL and abs(diag.j_max / gold["j_max"] - 1) < RTOL
+    assert diag.termination_reason == gold["reason"]
+    moved = P.transport_labels(l0c, v, cfg.transport())
+    assert abs(P.dice_averages(moved, l1c).d_a - gold["dice_post"]) <= 0.005
+    assert abs(P.dice_averages(l0c, l1c).d_a - gold["dice_pre"]) < 1e-12

@@ -167,3 +167,20 @@ def test_gpu_experiment(G, inputs):
             assert abs(getattr(r, k) - gr[k]) <= 0.005, k
         assert v.grid.dims == g.dims
         assert abs(float(np.linalg.norm(v.numpy())) / vl2 - 1) < 1e-2
+
+
+@pytest.mark.gpu
+def test_gpu_device_generator_matches_host():
+    """synth.c2_problem_device (the C4 tool's 1024^3 input path) == c2_problem."""
+    from paper_2209_08189_b200.synth import c2_problem, c2_problem_device
+    g = P.make_grid((32, 32, 32))
+    host = c2_problem(g, "linear", 4)
+    dev = c2_problem_device(g, "linear", 4)
+    assert torch_equal(host[2].labels, dev[2].labels) and torch_equal(host[3].labels, dev[3].labels)
+    for a, b in ((host[0].values, dev[0].values), (host[1].values, dev[1].values), (host[4].data, dev[4].data)):
+        assert float((a - b).abs().max()) < 1e-6
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
