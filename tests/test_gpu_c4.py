@@ -29,6 +29,7 @@ def test_c4_level4_matches_reference():
     m0c, m1c, l0c, l1c = (P.restrict(f, 4) for f in (m0, m1, l0, l1))
     del m0, m1, l0, l1
     torch.cuda.empty_cache()
+    assert hashlib.sha256(m0c.numpy().tobytes()).hexdigest() == gold["m0_sha256"]
     assert hashlib.sha256(m1c.numpy().tobytes()).hexdigest() == gold["m1_sha256"]
     assert hashlib.sha256(l1c.numpy().tobytes()).hexdigest() == gold["labels1_sha256"]
     cfg = P.RegistrationConfig(**gold["config"])

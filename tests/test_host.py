@@ -15,7 +15,9 @@ def test_public_names_match_reference_surface():
                  "ArmijoConfig", "ObjectiveState", "RegistrationConfig", "SolverDiagnostics",
                  "evaluate_objective", "gauss_newton_register", "hessian_matvec", "pcg_solve",
                  "reduced_gradient", "relative_residual", "make_reference", "make_velocity", "transport_labels",
-                 "DiceReport", "dice", "dice_averages", "jacobian_stats", "residual_image", "register"]:
+                 "DiceReport", "dice", "dice_averages", "jacobian_stats", "residual_image", "register", "SearchConfig", "SearchResult",
+                 "continuation_register", "in_bounds", "search_beta_v", "search_beta_w", "search_parameters",
+                 "ExperimentPlan", "run_experiment"]:
         assert hasattr(P, name), name
 
 
