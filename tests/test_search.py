@@ -184,3 +184,15 @@ def test_gpu_device_generator_matches_host():
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+@pytest.mark.gpu
+def test_gpu_in_bounds():
+    g = P.make_grid((16, 16, 16))
+    j = np.full(g.dims, 1.0, np.float32)
+    j[3, 4, 5] = 0.3
+    assert not P.in_bounds(P.ScalarField(g, j), 0.5) and P.in_bounds(P.ScalarField(g, j), 0.25)
+    j[3, 4, 5], j[0, 0, 0] = 1.0, 3.5
+    assert not P.in_bounds(P.ScalarField(g, j), 0.25) and P.in_bounds(P.ScalarField(g, j), 0.2)
+    with pytest.raises(ValueError):
+        P.in_bounds(P.ScalarField(g, j), 1.0)
