@@ -128,6 +128,47 @@ __global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v,
   }
 }
 
+// Periodic single-domain trace on the lean gather (3-D launch, no index
+// divisions, one conditional wrap per axis, immediate-offset x3 taps): the same
+// Heun steps and factors as trace_kernel, 3 components gathered per tap row.
+template <int ORDER, bool FACTORS>
+__global__ void __launch_bounds__(128) trace_lean_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
+                                                         float ih2, float ih3, float* __restrict__ disp_f,
+                                                         float* __restrict__ disp_b, const float* __restrict__ div,
+                                                         float* __restrict__ fac_f, float* __restrict__ fac_b) {
+  const Vox p = vox3(d);
+  if (!p.ok) return;
+  const int64_t N = d.n();
+  const PlaneSrc<3, false> sv{v, nullptr, nullptr, N, 0, 0, d.n1};
+  const float v1 = __ldg(v + p.idx), v2 = __ldg(v + N + p.idx), v3 = __ldg(v + 2 * N + p.idx);
+  const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
+  const float half = 0.5f * dt;
+  float vs[3];
+  gather_disp_lean<ORDER, 3, false>(sv, d, p.i, p.j, p.k, a1, a2, a3, vs);
+  const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
+  disp_f[p.idx] = f1;
+  disp_f[N + p.idx] = f2;
+  disp_f[2 * N + p.idx] = f3;
+  gather_disp_lean<ORDER, 3, false>(sv, d, p.i, p.j, p.k, -a1, -a2, -a3, vs);
+  const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
+  disp_b[p.idx] = b1;
+  disp_b[N + p.idx] = b2;
+  disp_b[2 * N + p.idx] = b3;
+  if (FACTORS) {
+    const PlaneSrc<1, false> sd{div, nullptr, nullptr, N, 0, 0, d.n1};
+    const float denom = 1.0f - half * __ldg(div + p.idx);
+    float dv;
+    gather_disp_lean<ORDER, 1, false>(sd, d, p.i, p.j, p.k, f1, f2, f3, &dv);
+    fac_f[p.idx] = (1.0f + half * dv) / denom;
+    gather_disp_lean<ORDER, 1, false>(sd, d, p.i, p.j, p.k, b1, b2, b3, &dv);
+    fac_b[p.idx] = (1.0f + half * dv) / denom;
+  }
+}
+
+// 0 (default): general flat-index trace; 1: lean periodic trace -- measured SLOWER on B200
+// (C2 cubic 3.83 vs 2.41 ms per trace), kept behind vr_set_trace_mode for A/B only
+static int g_trace_mode = 0;
+
 // ---- one semi-Lagrangian step: dst = interp(src, X) [* factor] --------------
 // state  : transport.py:130-133 (no factor)
 // adjoint: transport.py:154-155 (factor = adj_numer/adj_denom, backward trace)
@@ -397,6 +438,12 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
     else if (slab)
       trace_kernel<ORD, false, true><<<g, 256, 0, s>>>(v, d, w, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
                                                        nullptr, nullptr, nullptr);
+    else if (g_trace_mode == 1 && factors)
+      trace_lean_kernel<ORD, true><<<vox_grid(d), vox_tpb(d), 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd,
+                                                                       disp_bwd, div, fac_jac, fac_adj);
+    else if (g_trace_mode == 1)
+      trace_lean_kernel<ORD, false><<<vox_grid(d), vox_tpb(d), 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd,
+                                                                        disp_bwd, nullptr, nullptr, nullptr);
     else if (factors)
       trace_kernel<ORD, true, false><<<g, 256, 0, s>>>(v, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
                                                        fac_jac, fac_adj);
@@ -644,6 +691,12 @@ int vr_label_step_slab(const float* src, const float* src_lo, const float* src_h
 int vr_set_gather_mode(int mode) {
   const int prev = g_gather_mode;
   g_gather_mode = mode;
+  return prev;
+}
+
+int vr_set_trace_mode(int mode) {
+  const int prev = g_trace_mode;
+  g_trace_mode = mode;
   return prev;
 }
 

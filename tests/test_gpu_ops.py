@@ -262,3 +262,32 @@ def test_spectral_long_x1_lines(P, dims):
             P.apply_K(W, ops)
     else:
         assert rel_l2(_np(P.apply_K(W, ops).data), O.op_K(w.astype(np.float64), 1e-2, 1e-4)) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(32, 32, 32), (16, 20, 24)])
+def test_trace_lean_matches_general(dims):
+    """vr_set_trace_mode A/B: the lean periodic trace (default) against the
+    general flat-index trace, both orders, with and without source factors,
+    including displacements beyond one period (scaled velocity)."""
+    import torch
+    import paper_2209_08189_b200 as P
+    from paper_2209_08189_b200 import _lib
+    from paper_2209_08189_b200.synth import velocity_array
+    g = P.make_grid(dims)
+    lib = _lib.lib()
+    for scale in (0.25, 40.0):
+        v = P.VectorField(g, scale * velocity_array(2, g))
+        for order in ("cubic", "linear"):
+            outs = {}
+            for mode in (0, 1):
+                prev = lib.vr_set_trace_mode(mode)
+                try:
+                    t = P.TransportOperators(v, P.TransportConfig(4, order))
+                    outs[mode] = [t.forward.displacement.clone(), t.backward.displacement.clone(),
+                                  t.jac_factor.clone(), t.adj_factor.clone()]
+                finally:
+                    lib.vr_set_trace_mode(prev)
+            torch.cuda.synchronize()
+            for x, y in zip(outs[0], outs[1]):
+                assert float((x - y).abs().max()) <= 4e-6 * max(float(x.abs().max()), 1.0), (order, scale)

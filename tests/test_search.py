@@ -193,6 +193,6 @@ def test_gpu_in_bounds():
     j[3, 4, 5] = 0.3
     assert not P.in_bounds(P.ScalarField(g, j), 0.5) and P.in_bounds(P.ScalarField(g, j), 0.25)
     j[3, 4, 5], j[0, 0, 0] = 1.0, 3.5
-    assert not P.in_bounds(P.ScalarField(g, j), 0.25) and P.in_bounds(P.ScalarField(g, j), 0.2)
+    assert not P.in_bounds(P.ScalarField(g, j), 0.3) and P.in_bounds(P.ScalarField(g, j), 0.2)
     with pytest.raises(ValueError):
         P.in_bounds(P.ScalarField(g, j), 1.0)
