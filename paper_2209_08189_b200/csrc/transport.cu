@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v,
 // divisions, one conditional wrap per axis, immediate-offset x3 taps): the same
 // Heun steps and factors as trace_kernel, 3 components gathered per tap row.
 template <int ORDER, bool FACTORS>
-__global__ void __launch_bounds__(128) trace_lean_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
+__global__ void __launch_bounds__(128, 5) trace_lean_kernel(const float* __restrict__ v, Dims d, float dt, float ih1,
                                                          float ih2, float ih3, float* __restrict__ disp_f,
                                                          float* __restrict__ disp_b, const float* __restrict__ div,
                                                          float* __restrict__ fac_f, float* __restrict__ fac_b) {
