@@ -55,10 +55,15 @@ __global__ void __launch_bounds__(256) interp_points_kernel(const float* __restr
   // index = p / h (interp.py:23-25), floor, fraction; computed in f64
   double q1 = (double)pts[p] / h1, q2 = (double)pts[npts + p] / h2, q3 = (double)pts[2 * npts + p] / h3;
   double f1 = floor(q1), f2 = floor(q2), f3 = floor(q3);
-  SrcF32 s{{src, src, src}, 0};
+  // base index into [0,n) (a full modulo only off the principal period), then
+  // the lean gather: one row pointer per stencil row, immediate-offset taps
+  int ix = (int)f1, iy = (int)f2, iz = (int)f3;
+  if ((unsigned)ix >= (unsigned)d.n1) ix = wrap_idx(ix, d.n1);
+  if ((unsigned)iy >= (unsigned)d.n2) iy = wrap_idx(iy, d.n2);
+  if ((unsigned)iz >= (unsigned)d.n3) iz = wrap_idx(iz, d.n3);
+  const PlaneSrc<1, false> s{src, nullptr, nullptr, d.n(), 0, 0, d.n1};
   float o;
-  gather<ORDER, 1>(s, d, (int)f1, (int)f2, (int)f3, (float)(q1 - f1), (float)(q2 - f2), (float)(q3 - f3),
-                   &o);
+  gather_lean<ORDER, 1, false>(s, d, ix, iy, iz, (float)(q1 - f1), (float)(q2 - f2), (float)(q3 - f3), &o);
   out[p] = o;
 }
 
