@@ -17,6 +17,11 @@
  *    voxels.
  *  - Characteristics are displacements in index units: the departure point of
  *    voxel (i,j,k) is (i-d1, j-d2, k-d3).
+ *  - Alignment: field pointers need only 4-byte (float) alignment.  The
+ *    shared-memory-staged cubic sweeps (cp.async.bulk) are used only when the
+ *    source pointers (src / ghost blocks) are 16-byte aligned; otherwise the
+ *    direct gather runs (same results).  torch / cudaMalloc allocations are
+ *    256-byte aligned.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All calls are
  *    asynchronous; reductions write f64 results to device memory.
  *  - Return 0 on success, negative VR_ERR_* on invalid arguments / launch
@@ -158,6 +163,11 @@ int vr_vecstats(const float* v, int64_t n, double* scratch, double* out4, void* 
 int vr_axpby(int64_t n, double a, const float* x, double b, const float* y, float* out, void* stream);
 int vr_pcg_update(int64_t n, double alpha, const float* p, const float* hp, float* x, float* r, void* stream);
 int vr_fill(int64_t n, float value, float* out, void* stream);
+
+/* (min l0, max l0, min l1, max l1) of one or two int32 label maps (l1 may be
+ * NULL), written to out[4] (int32, device).  Validates label ids (grid.py
+ * LabelMap, non-negative) and sizes vr_label_counts with one host read. */
+int vr_label_range(const int* l0, const int* l1, int64_t n, int* out, void* stream);
 
 /* ---- Dice counts (metrics.py:45-57,72-73) ------------------------------------
  * counts[3*id+{0,1,2}] = |l0==id|, |l1==id|, |l0==id & l1==id|, id <= max_id */

@@ -60,6 +60,7 @@ _SIGS = {
     "vr_pcg_update": [_i64, _f64, _p, _p, _p, _p, _p],
     "vr_fill": [_i64, _f32, _p, _p],
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
+    "vr_label_range": [_p, _p, _i64, _p, _p],
     # x1-slab / distributed
     "vr_trace_rk2_slab": [_p, _dims_t, _i64, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
     "vr_advect_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _i32, _p, _p, _i32, _i32, _p],
@@ -88,7 +89,7 @@ class NativeError(VelregError):
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches accounting)
-LAUNCHES = {"vr_spec_apply": 5, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2,
+LAUNCHES = {"vr_spec_apply": 5, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
             "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
@@ -243,7 +244,9 @@ def defer_check(flag: torch.Tensor, exc: Exception) -> None:
 
 
 def is_deferred(flag: torch.Tensor) -> bool:
-    return any(f is flag for f, _ in _deferred)
+    # match on storage: callers take fresh views (flags[slot]) of the same word
+    p = flag.data_ptr()
+    return any(f.data_ptr() == p for f, _ in _deferred)
 
 
 def run_deferred() -> None:

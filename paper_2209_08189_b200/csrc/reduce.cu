@@ -13,6 +13,7 @@
 // CTA, then one CTA sums the partials in index order), so results are
 // bit-reproducible run to run -- the analogue of the reference's
 // "reproducible" serial kernels (runtime.py:1-17).
+#include <climits>
 #include "common.cuh"
 #include "../../include/velreg_b200.h"
 
@@ -20,6 +21,11 @@ namespace vr {
 
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocks = 148 * 4;  // one wave of 4 CTAs per SM
+
+// NaN-propagating min / max (numpy .min() / .max() return NaN when any entry
+// is NaN; fmin / fmax would skip it and let a NaN Jacobian pass in_bounds)
+__device__ __forceinline__ double nmin(double x, double y) { return x != x ? x : (y != y ? y : fmin(x, y)); }
+__device__ __forceinline__ double nmax(double x, double y) { return x != x ? x : (y != y ? y : fmax(x, y)); }
 
 template <int K>
 __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* __restrict__ dst, int mode) {
@@ -30,7 +36,7 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* __res
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = (mode == VR_RED_SUM) ? x + y : (((q & 1) == 0) ? fmin(x, y) : fmax(x, y));
+      x = (mode == VR_RED_SUM) ? x + y : (((q & 1) == 0) ? nmin(x, y) : nmax(x, y));
     }
     if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = x;
   }
@@ -40,7 +46,7 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[K], double* __res
     for (int q = 0; q < K; ++q) {
       double x = red[q][0];
       for (int w = 1; w < kRedThreads / 32; ++w)
-        x = (mode == VR_RED_SUM) ? x + red[q][w] : (((q & 1) == 0) ? fmin(x, red[q][w]) : fmax(x, red[q][w]));
+        x = (mode == VR_RED_SUM) ? x + red[q][w] : (((q & 1) == 0) ? nmin(x, red[q][w]) : nmax(x, red[q][w]));
       dst[q] = x;
     }
   }
@@ -93,12 +99,12 @@ __global__ void __launch_bounds__(kRedThreads) minmax_partials_kernel(const floa
   double acc[4] = {INFINITY, -INFINITY, INFINITY, -INFINITY};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double x = __ldg(a + i);
-    acc[0] = fmin(acc[0], x);
-    acc[1] = fmax(acc[1], x);
+    acc[0] = nmin(acc[0], x);
+    acc[1] = nmax(acc[1], x);
     if (b) {
       const double y = __ldg(b + i);
-      acc[2] = fmin(acc[2], y);
-      acc[3] = fmax(acc[3], y);
+      acc[2] = nmin(acc[2], y);
+      acc[3] = nmax(acc[3], y);
     }
   }
   block_reduce_store<4>(acc, partials + (int64_t)blockIdx.x * 4, VR_RED_MINMAX);
@@ -139,12 +145,12 @@ __global__ void fold_partials_kernel(const double* __restrict__ partials, int nb
     double x = (mode == VR_RED_SUM) ? 0.0 : (isMin ? INFINITY : -INFINITY);
     for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
       const double y = partials[(int64_t)b * stride + q];
-      x = (mode == VR_RED_SUM) ? x + y : (isMin ? fmin(x, y) : fmax(x, y));
+      x = (mode == VR_RED_SUM) ? x + y : (isMin ? nmin(x, y) : nmax(x, y));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = (mode == VR_RED_SUM) ? x + y : (isMin ? fmin(x, y) : fmax(x, y));
+      x = (mode == VR_RED_SUM) ? x + y : (isMin ? nmin(x, y) : nmax(x, y));
     }
     if (lane == 0) red[q][w] = x;
   }
@@ -154,7 +160,7 @@ __global__ void fold_partials_kernel(const double* __restrict__ partials, int nb
     const bool isMin = (mode == VR_RED_MINMAX) && ((q & 1) == 0);
     double x = red[q][0];
     for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
-      x = (mode == VR_RED_SUM) ? x + red[q][ww] : (isMin ? fmin(x, red[q][ww]) : fmax(x, red[q][ww]));
+      x = (mode == VR_RED_SUM) ? x + red[q][ww] : (isMin ? nmin(x, red[q][ww]) : nmax(x, red[q][ww]));
     out[q] = x;
   }
 }
@@ -203,6 +209,41 @@ __global__ void __launch_bounds__(256) label_counts_kernel(const int* __restrict
   __syncthreads();
   for (int t = threadIdx.x; t < nb; t += blockDim.x)
     if (hist[t]) atomicAdd(counts + t, (unsigned long long)hist[t]);
+}
+
+// (min l0, max l0, min l1, max l1) of one or two int32 label maps in one pass:
+// validates label ids (grid.py LabelMap: non-negative) and sizes the label
+// histogram with a single host read.  Integer min / max atomics are
+// order-independent, so the result is deterministic.
+__global__ void label_range_init_kernel(int* __restrict__ out) {
+  if (threadIdx.x < 4) out[threadIdx.x] = (threadIdx.x & 1) ? INT_MIN : INT_MAX;
+}
+
+__global__ void __launch_bounds__(256) label_range_kernel(const int* __restrict__ l0, const int* __restrict__ l1,
+                                                          int64_t n, int* __restrict__ out) {
+  int a0 = INT_MAX, a1 = INT_MIN, b0 = INT_MAX, b1 = INT_MIN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = __ldg(l0 + i);
+    a0 = min(a0, a);
+    a1 = max(a1, a);
+    if (l1) {
+      const int b = __ldg(l1 + i);
+      b0 = min(b0, b);
+      b1 = max(b1, b);
+    }
+  }
+  a0 = __reduce_min_sync(~0u, a0);
+  a1 = __reduce_max_sync(~0u, a1);
+  b0 = __reduce_min_sync(~0u, b0);
+  b1 = __reduce_max_sync(~0u, b1);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, a0);
+    atomicMax(out + 1, a1);
+    if (l1) {
+      atomicMin(out + 2, b0);
+      atomicMax(out + 3, b1);
+    }
+  }
 }
 
 }  // namespace vr
@@ -296,6 +337,15 @@ int vr_fill(int64_t n, float value, float* out, void* stream) {
   if (!out || n < 0) return VR_ERR_ARG;
   if (n == 0) return VR_OK;
   fill_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(n, value, out);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_label_range(const int* l0, const int* l1, int64_t n, int* out, void* stream) {
+  if (!l0 || !out || n < 0) return VR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  label_range_init_kernel<<<1, 32, 0, s>>>(out);
+  if (n > 0) label_range_kernel<<<red_blocks(n), 256, 0, s>>>(l0, l1, n, out);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }

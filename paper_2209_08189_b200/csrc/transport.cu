@@ -464,8 +464,13 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
 // vr_set_gather_mode(0) selects the direct per-point kernels (A/B checks).
 static int g_gather_mode = 1;
 // Cubic only: the trilinear sweep (8 taps, 2.7 TB/s direct) measured slower staged.
-static bool use_staged(int order, const Dims& d) {
-  return g_gather_mode == 1 && order == ORDER_CUBIC && stg::staged_ok(d);
+// cp.async.bulk needs 16-byte-aligned global rows: the row offsets are
+// multiples of 128 B (n3 % 32 == 0, x3 start a multiple of 4 floats), so the
+// field base pointers decide; anything less aligned takes the direct gather.
+static bool use_staged(int order, const Dims& d, const float* src, const float* lo = nullptr,
+                       const float* hi = nullptr) {
+  const uintptr_t a = (uintptr_t)src | (uintptr_t)lo | (uintptr_t)hi;
+  return g_gather_mode == 1 && order == ORDER_CUBIC && stg::staged_ok(d) && (a & 15) == 0;
 }
 
 template <int ORD, bool SLAB, class Epi>
@@ -487,7 +492,7 @@ static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], con
   if (x0 < 0 || nx < 0 || x0 + nx > d.n1) return VR_ERR_ARG;
   if (nx == 0) return VR_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (use_staged(order, d)) {
+  if (use_staged(order, d, src, sg.lo, sg.hi)) {
     VR_DISPATCH_ORDER(order, {
       if (sg.on()) {
         auto ps = slab_src<1>(src, sg.lo, sg.hi, 0, 0, sg.w, d.n1);
@@ -539,7 +544,7 @@ static int incstate_impl(const float* u, SlabArgs sg, const int64_t dims[3], con
   if (x0 < 0 || nx < 0 || x0 + nx > d.n1) return VR_ERR_ARG;
   if (nx == 0) return VR_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (use_staged(order, d)) {
+  if (use_staged(order, d, u, sg.lo, sg.hi)) {
     const IncEpi epi{vt, gradm_next, d.n(), (float)(0.5 * dt), last, out, nonfinite_flag};
     VR_DISPATCH_ORDER(order, {
       if (sg.on())

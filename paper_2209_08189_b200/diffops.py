@@ -220,7 +220,7 @@ _ws_cache: dict = {}
 
 def workspace_for(grid: Grid):
     from . import dist
-    ctx = dist.current()
+    ctx = dist.for_grid(grid.dims)
     key = (grid.dims, torch.cuda.current_device(), id(ctx) if ctx is not None else None)
     ws = _ws_cache.get(key)
     if ws is None:
@@ -260,7 +260,7 @@ def fd8_gradient_t(f: torch.Tensor, out: torch.Tensor | None = None) -> torch.Te
     dims = tuple(f.shape[-3:])
     if out is None:
         out = torch.empty((3,) + dims, dtype=torch.float32, device=f.device)
-    ctx = dist.current()
+    ctx = dist.for_shape(f.shape)
     if ctx is not None:   # x1 slab: 4 ghost planes from the neighbours
         lo, hi = ctx.ghosts(f, 4)
         _lib.check(_lib.lib().vr_fd8_grad_slab(f.data_ptr(), lo.data_ptr(), hi.data_ptr(), _lib.dims_arg(dims),
@@ -276,7 +276,7 @@ def fd8_divergence_t(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.
     dims = tuple(v.shape[-3:])
     if out is None:
         out = torch.empty(dims, dtype=torch.float32, device=v.device)
-    ctx = dist.current()
+    ctx = dist.for_shape(v.shape)
     if ctx is not None:   # only v1 is differentiated along x1
         lo, hi = ctx.ghosts(v[0], 4)
         _lib.check(_lib.lib().vr_fd8_div_slab(v.data_ptr(), lo.data_ptr(), hi.data_ptr(), _lib.dims_arg(dims),

@@ -36,6 +36,26 @@ def current():
     return _CTX
 
 
+def for_grid(dims):
+    """The active context if it decomposes a lattice of `dims`, else None (a
+    field on another grid is single-domain even while a context is active)."""
+    ctx = _CTX
+    if ctx is not None and tuple(ctx.dims) == tuple(int(n) for n in dims):
+        return ctx
+    return None
+
+
+def for_shape(shape):
+    """The active context if a tensor of `shape` (..., L1, N2, N3) is one of its
+    local slabs, else None.  Every slab-aware operator and reduction routes
+    through this (or `for_grid`), so one call never mixes slab kernels with a
+    replicated field."""
+    ctx = _CTX
+    if ctx is not None and len(shape) >= 3 and tuple(shape[-3:]) == tuple(ctx.local_dims):
+        return ctx
+    return None
+
+
 @contextlib.contextmanager
 def activate(ctx):
     global _CTX
@@ -157,3 +177,10 @@ def ghost_width(vmax1: float, dt: float, n1: int, order: str) -> int:
     """x1 ghost planes covering every departure point plus the stencil."""
     h1 = 2 * math.pi / n1
     return max(4, int(math.ceil(dt * vmax1 / h1)) + (3 if order == "cubic" else 2))
+
+
+def ghost_width_for_displacement(dmax1: float, order: str) -> int:
+    """Smallest ghost width whose planes hold every departure stencil of x1
+    displacement |d1| <= dmax1: the slab gathers accept base indices in
+    [1 - w, L1 + w - 3] (cubic) / [-w, L1 + w - 2] (linear)."""
+    return int(math.ceil(dmax1)) + (1 if order == "cubic" else 0)

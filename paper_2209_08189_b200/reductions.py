@@ -15,10 +15,14 @@ def _n(t: torch.Tensor) -> int:
     return t.numel()
 
 
-def _sum(out: torch.Tensor) -> np.ndarray:
+def _ctx(t: torch.Tensor):
+    """The slab context `t` belongs to (dist.for_shape), or None."""
+    return _dist.for_shape(t.shape)
+
+
+def _sum(out: torch.Tensor, ctx) -> np.ndarray:
     """Host copy of a device result vector, summed across ranks (on device) when
-    a slab decomposition is active."""
-    ctx = _dist.current()
+    the operands are slabs of an active decomposition."""
     if ctx is not None:
         ctx.allreduce_(out, "sum")
     res = out.cpu().numpy()
@@ -36,7 +40,7 @@ def dots(pairs) -> np.ndarray:
     a = _lib.ptr_array([p[0] for p in pairs])
     b = _lib.ptr_array([p[1] for p in pairs])
     _lib.check(lib.vr_dots(k, a, b, n, _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()), "vr_dots")
-    return _sum(out)
+    return _sum(out, _ctx(pairs[0][0]))
 
 
 def dot(a: torch.Tensor, b: torch.Tensor) -> float:
@@ -48,7 +52,7 @@ def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> n
     out = _lib.out_buf(2)
     _lib.check(lib.vr_sqdiff(a.data_ptr(), b.data_ptr(), _lib.ptr(c), _n(a), _lib.scratch().data_ptr(),
                              out.data_ptr(), _lib.stream()), "vr_sqdiff")
-    return _sum(out)
+    return _sum(out, _ctx(a))
 
 
 def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
@@ -56,7 +60,7 @@ def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
     out = _lib.out_buf(4)
     _lib.check(lib.vr_minmax(a.data_ptr(), _lib.ptr(b), _n(a), _lib.scratch().data_ptr(), out.data_ptr(),
                              _lib.stream()), "vr_minmax")
-    ctx = _dist.current()
+    ctx = _ctx(a)
     if ctx is not None:
         out[0::2].neg_()
         ctx.allreduce_(out, "max")
@@ -70,11 +74,12 @@ def local_absmax(x: torch.Tensor) -> float:
     return max(abs(mn), abs(mx))
 
 
-def minmax_local(a: torch.Tensor) -> np.ndarray:
+def minmax_local(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
+    """(min a, max a, min b, max b) over this rank's data only (no allreduce)."""
     lib = _lib.lib()
     out = _lib.out_buf(4)
-    _lib.check(lib.vr_minmax(a.data_ptr(), None, _n(a), _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()),
-               "vr_minmax")
+    _lib.check(lib.vr_minmax(a.data_ptr(), _lib.ptr(b), _n(a), _lib.scratch().data_ptr(), out.data_ptr(),
+                             _lib.stream()), "vr_minmax")
     return out.cpu().numpy()
 
 
@@ -84,7 +89,7 @@ def vecstats(v: torch.Tensor) -> tuple:
     out = _lib.out_buf(4)
     _lib.check(lib.vr_vecstats(v.data_ptr(), _n(v) // 3, _lib.scratch().data_ptr(), out.data_ptr(),
                                _lib.stream()), "vr_vecstats")
-    ctx = _dist.current()
+    ctx = _ctx(v)
     if ctx is not None:
         ctx.allreduce_(out[1:2], "max")
         ctx.allreduce_(out[2:4], "sum")
@@ -112,13 +117,28 @@ def fill(out: torch.Tensor, value: float) -> torch.Tensor:
     return out
 
 
+def label_range(l0: torch.Tensor, l1: torch.Tensor | None = None) -> np.ndarray:
+    """(min l0, max l0, min l1, max l1) over the whole decomposed field (one
+    device pass, one host read); int32 extremes for an absent / empty map."""
+    out = torch.empty(4, dtype=torch.int32, device=l0.device)
+    _lib.check(_lib.lib().vr_label_range(l0.data_ptr(), _lib.ptr(l1), _n(l0), out.data_ptr(), _lib.stream()),
+               "vr_label_range")
+    ctx = _ctx(l0)
+    if ctx is not None:
+        o = out.to(torch.float64)
+        o[0::2].neg_()
+        ctx.allreduce_(o, "max")
+        o[0::2].neg_()
+        return o.cpu().numpy().astype(np.int64)
+    return out.cpu().numpy().astype(np.int64)
+
+
 def label_histogram(l0: torch.Tensor, l1: torch.Tensor, max_id: int | None = None) -> np.ndarray:
     """counts[id] = (|l0==id|, |l1==id|, |l0==id & l1==id|) as exact int64."""
-    ctx = _dist.current()
+    ctx = _ctx(l0)
     if max_id is None:
-        max_id = int(max(int(l0.max()), int(l1.max()))) if l0.numel() else 0
-        if ctx is not None:
-            max_id = int(ctx.allreduce([max_id], "max")[0])
+        r = label_range(l0, l1)
+        max_id = max(int(r[1]), int(r[3]), 0) if l0.numel() else 0
     counts = torch.empty(3 * (max_id + 1), dtype=torch.int64, device=l0.device)
     _lib.check(_lib.lib().vr_label_counts(l0.data_ptr(), l1.data_ptr(), _n(l0), int(max_id), counts.data_ptr(),
                                           _lib.stream()), "vr_label_counts")

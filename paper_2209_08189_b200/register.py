@@ -11,6 +11,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import torch
+
 from .grid import Grid, LabelMap, ScalarField, VectorField
 from .metrics import DiceReport, dice_averages
 from .optim import RegistrationConfig, SolverDiagnostics, gauss_newton_solve
@@ -39,20 +41,55 @@ def _as_field(x, grid: Grid | None) -> ScalarField:
     return ScalarField(grid, x)
 
 
+_side = {}
+
+
+def _upload_async(items, pending: list) -> list:
+    """Copy pinned host tensors to the device on a side stream (overlapping the
+    Gauss-Newton solve); the caller's stream waits on the returned events
+    before first use.  Anything else is returned unchanged."""
+    out = []
+    for x in items:
+        if isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.is_pinned() and x.dtype == torch.int32:
+            dev = torch.cuda.current_device()
+            st = _side.get(dev)
+            if st is None:
+                st = _side[dev] = torch.cuda.Stream()
+            d = torch.empty(x.shape, dtype=torch.int32, device="cuda")
+            st.wait_stream(torch.cuda.current_stream())   # d's allocation is ordered on the current stream
+            with torch.cuda.stream(st):
+                d.copy_(x, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(st)
+            pending.append(ev)
+            out.append(d)
+        else:
+            out.append(x)
+    return out
+
+
 def register(m0, m1, params: RegistrationConfig | dict | None = None, labels0=None, labels1=None,
-             v0: VectorField | None = None, pre_dice: bool = False) -> RegistrationResult:
-    """Register template m0 to reference m1 (arrays, tensors or ScalarFields)."""
+             v0: VectorField | None = None, pre_dice: bool = False, grid: Grid | None = None) -> RegistrationResult:
+    """Register template m0 to reference m1 (arrays, tensors or ScalarFields;
+    pinned host tensors are uploaded asynchronously).  `grid` names the lattice
+    when m0 is a bare array that is only this rank's x1 slab."""
     if params is None:
         cfg = RegistrationConfig()
     elif isinstance(params, dict):
         cfg = RegistrationConfig(**params)
     else:
         cfg = params
-    m0 = _as_field(m0, None)
+    m0 = _as_field(m0, grid)
     m1 = _as_field(m1, m0.grid)
+    # host label maps (pinned) upload on a side stream while the solver runs
+    pending = []
+    if labels0 is not None and labels1 is not None:
+        labels0, labels1 = _upload_async([labels0, labels1], pending)
     v, diag, state = gauss_newton_solve(m0, m1, cfg, v0)
     res = RegistrationResult(v, state.deformed, diag.relative_residual, diag)
     if labels0 is not None and labels1 is not None:
+        for ev in pending:
+            torch.cuda.current_stream().wait_event(ev)
         l0 = labels0 if isinstance(labels0, LabelMap) else LabelMap(m0.grid, labels0)
         l1 = labels1 if isinstance(labels1, LabelMap) else LabelMap(m0.grid, labels1)
         moved = transport_labels(l0, v, cfg.transport(), state.transport_ops)

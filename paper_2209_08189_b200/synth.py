@@ -29,8 +29,8 @@ def _coords(grid: Grid) -> np.ndarray:
     """Lattice coordinates of this rank's part of `grid` (all of it unless an
     x1-slab decomposition is active)."""
     from . import dist
-    ctx = dist.current()
-    if ctx is not None and tuple(ctx.dims) == tuple(grid.dims):
+    ctx = dist.for_grid(grid.dims)
+    if ctx is not None:
         return ctx.local_coords()
     return grid.coords()
 
@@ -74,7 +74,7 @@ def transport_labels(labels: LabelMap, v: VectorField, cfg: TransportConfig,
                     _lib.check(lib.vr_label_step_slab(cur.data_ptr(), lo.data_ptr(), hi.data_ptr(), int(lab), d,
                                                       ops.w, disp, order, None, out.data_ptr(), st),
                                "vr_label_step_slab")
-        return LabelMap(labels.grid, out)
+        return LabelMap(labels.grid, out, labels.max_id)
     for lab in labels.label_ids():
         src = None
         for j in range(cfg.n_t):
@@ -85,7 +85,7 @@ def transport_labels(labels: LabelMap, v: VectorField, cfg: TransportConfig,
                                    out.data_ptr() if last else None, st)
             _lib.check(rc, "vr_label_step")
             src = dst
-    return LabelMap(labels.grid, out)
+    return LabelMap(labels.grid, out, labels.max_id)
 
 
 def make_reference(m0: ScalarField, labels: LabelMap, v: VectorField, cfg: TransportConfig):

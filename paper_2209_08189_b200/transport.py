@@ -10,6 +10,7 @@ n_t steps and reads the non-finite flag where the reference checks
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import torch
@@ -127,8 +128,7 @@ class TransportOperators:
         self.v = v
         self.cfg = cfg
         self.grid = v.grid
-        ctx = _dist.current()
-        self.ctx = ctx if ctx is not None and tuple(ctx.dims) == tuple(v.grid.dims) else None
+        self.ctx = _dist.for_grid(v.grid.dims)
         if self.ctx is None:
             self.div = fd8_divergence_t(v.data)
             disp_f, disp_b, self.jac_factor, self.adj_factor = _trace(v.data, v.grid.dims, cfg.dt, cfg.interp_order,
@@ -146,23 +146,42 @@ class TransportOperators:
         """Ghost width from the global max |v1| (allreduce), one halo exchange
         of v (covers both the FD8 divergence and the RK2 star points), one of
         div (for the source factors), then the slab trace kernel."""
-        from .reductions import local_absmax
+        from .reductions import local_absmax, minmax_local
         ctx, cfg = self.ctx, self.cfg
         vmax1 = float(ctx.allreduce([local_absmax(v[0])], "max")[0])
-        self.w = _dist.ghost_width(vmax1, cfg.dt, self.grid.dims[0], cfg.interp_order)
+        w = _dist.ghost_width(vmax1, cfg.dt, self.grid.dims[0], cfg.interp_order)
         ldims = ctx.local_dims
         self.div = fd8_divergence_t(v)
-        v_ext = ctx.halo(v, self.w)          # contiguous ghost-extended copies, once per iterate
-        d_ext = ctx.halo(self.div, self.w)
         disp_f = torch.empty_like(v)
         disp_b = torch.empty_like(v)
         self.jac_factor = torch.empty_like(self.div)
         self.adj_factor = torch.empty_like(self.div)
-        _lib.check(_lib.lib().vr_trace_rk2_slab(v_ext.data_ptr(), _lib.dims_arg(ldims), ctx.dims[0], self.w,
-                                                float(cfg.dt), _order(cfg.interp_order), disp_f.data_ptr(),
-                                                disp_b.data_ptr(), d_ext.data_ptr(), self.jac_factor.data_ptr(),
-                                                self.adj_factor.data_ptr(), _lib.stream()), "vr_trace_rk2_slab")
-        return disp_f, disp_b
+        while True:
+            self.w = w
+            v_ext = ctx.halo(v, w)          # contiguous ghost-extended copies, once per iterate
+            d_ext = ctx.halo(self.div, w)
+            _lib.check(_lib.lib().vr_trace_rk2_slab(v_ext.data_ptr(), _lib.dims_arg(ldims), ctx.dims[0], w,
+                                                    float(cfg.dt), _order(cfg.interp_order), disp_f.data_ptr(),
+                                                    disp_b.data_ptr(), d_ext.data_ptr(), self.jac_factor.data_ptr(),
+                                                    self.adj_factor.data_ptr(), _lib.stream()), "vr_trace_rk2_slab")
+            # The width above bounds the Heun star point by max|v1|, but the
+            # second stage uses the INTERPOLATED v(x*), which cubic Lagrange can
+            # overshoot.  The slab gathers clamp the x1 base index into the
+            # ghosts, so check the actual departure displacements (both traces,
+            # all ranks) and redo the trace with wider ghosts if any departure
+            # stencil -- or an interior-plane stencil of the overlapped sweeps --
+            # would leave the exchanged planes.
+            mn_f, mx_f, mn_b, mx_b = minmax_local(disp_f[0], disp_b[0])
+            dmax = float(ctx.allreduce([max(abs(mn_f), abs(mx_f), abs(mn_b), abs(mx_b))], "max")[0])
+            if not math.isfinite(dmax):
+                raise TransportError("characteristic trace produced non-finite displacements")
+            need = _dist.ghost_width_for_displacement(dmax, cfg.interp_order)
+            if need <= w:
+                return disp_f, disp_b
+            if need > ldims[0]:
+                raise TransportError(f"departure points travel {dmax:.1f} x1 planes, more than the slab depth "
+                                     f"{ldims[0]}; use fewer ranks or a larger n_t")
+            w = need
 
     def sweep(self, values: torch.Tensor, disp: torch.Tensor, factor: torch.Tensor | None = None,
               out: torch.Tensor | None = None, flag=None) -> torch.Tensor:
