@@ -84,6 +84,12 @@ int vr_set_gather_mode(int mode);
  * 0 = radix-8 Stockham kernels only.  Returns the previous mode. */
 int vr_set_fft_mode(int mode);
 
+/* Tuning switch (no reference counterpart) for VR_SPEC_A: 1 (default) = the
+ * separable f64 line engine (spectral_d2.cuh: A = D11 + D22 + D33, each a 1-D
+ * f64 transform pair per line, for line lengths 128 / 256), 0 = the 3-D path
+ * with an f64 forward half.  Returns the previous mode. */
+int vr_set_spec_a_mode(int mode);
+
 /* Tuning switch (no reference counterpart) for the single-domain RK2 trace:
  * 0 (default) = general flat-index gathers, 1 = lean periodic gathers on a 3-D
  * launch (measured slower: 3.83 vs 2.41 ms at C2 cubic).  Same taps; summation

@@ -36,6 +36,7 @@ _SIGS = {
     "vr_disp_to_points": [_p, _dims_t, _p, _p],
     "vr_set_gather_mode": [_i32],
     "vr_set_fft_mode": [_i32],
+    "vr_set_spec_a_mode": [_i32],
     "vr_set_trace_mode": [_i32],
     "vr_advect": [_p, _dims_t, _p, _p, _i32, _p, _p, _p],
     "vr_incstate_init": [_p, _p, _dims_t, _f64, _p, _p],

@@ -28,6 +28,8 @@
 #include <new>
 #include <type_traits>
 #include <algorithm>
+#include <mutex>
+#include <utility>
 #include "common.cuh"
 #include "../../include/velreg_b200.h"
 
@@ -494,10 +496,14 @@ __global__ void finalize_sum_kernel(const double* __restrict__ partials, int n, 
 
 #include "spectral_fast.cuh"
 #include "spectral_4step.cuh"
+#include "spectral_d2.cuh"
 
 // Four-step register FFT kernels (spectral_4step.cuh) for the line lengths they
 // cover; vr_set_fft_mode(0) selects the Stockham engine for A/B checks.
 static int g_fft_mode = 1;
+// A = |k|^2 through the separable f64 line engine (spectral_d2.cuh) where the
+// line lengths allow; vr_set_spec_a_mode(0) selects the 3-D f64 path.
+static int g_a_mode = 1;
 
 using namespace vr;
 
@@ -713,12 +719,21 @@ int vr_spec_plan_destroy(vr_spec_plan* p) {
 
 }  // extern "C"
 
+// Opt a kernel into `bytes` of dynamic shared memory once per (device, kernel,
+// size).  Keyed on the kernel's address: template instances that differ only
+// in non-type parameters share a function TYPE, so a per-type static flag
+// would skip the opt-in for all but the first of them.
 template <typename F> static void smem_optin(F* f, size_t bytes) {
-  static bool done = false;   // per instantiation
-  if (!done) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done = true;
-  }
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(f), dev};
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first == key && e.second >= bytes) return;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.push_back({key, bytes});
 }
 
 // strided c2c pass along x1 (axis 1) or x2 (axis 2) over ncomp spectra
@@ -898,7 +913,72 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   return nblk;
 }
 
+// ---- A via the separable line engine (spectral_d2.cuh) ------------------------------
+static int d2_r2(int L) { return L == 256 ? 16 : (L == 128 ? 8 : 0); }
+static int g_d2_threads = 128;   // CTA size of the line passes (128: 3 CTAs / SM at 160 registers)
+
+static bool d2_ok(const vr_spec_plan* p) {
+  const Dims& d = p->d;
+  const int r1 = d2_r2(d.n1), r2 = d2_r2(d.n2), r3 = d2_r2(d.n3);
+  return g_a_mode && r1 && r2 && r3 && d.n3 % 64 == 0 && d.n2 % 2 == 0;
+}
+
+template <int R2, int NT>
+static void d2_rows(vr_spec_plan* p, const float* in, float* acc, int ncomp, cudaStream_t s) {
+  const Dims& d = p->d;
+  constexpr size_t sm = d2::smem_bytes<R2, NT>();
+  smem_optin(d2::rows_kernel<R2, NT>, sm);
+  const int npairs = d.n1 * d.n2 / 2, lpb = NT / R2;
+  d2::rows_kernel<R2, NT><<<dim3((npairs + lpb - 1) / lpb, ncomp), NT, sm, s>>>(in, acc, npairs, d.n(), p->tw3,
+                                                                                1.0 / d.n3);
+}
+
+template <int R2, bool FINAL, int NT>
+static void d2_strided(vr_spec_plan* p, int axis, const float* in, float* acc, const float* add, float* out,
+                       int ncomp, double alpha, cudaStream_t s) {
+  const Dims& d = p->d;
+  constexpr size_t sm = d2::smem_bytes<R2, NT>();
+  smem_optin(d2::strided_kernel<R2, FINAL, NT>, sm);
+  const bool ax2 = axis == 2;
+  const int L = ax2 ? d.n2 : d.n1;
+  const int es = ax2 ? d.n3 : d.n2 * d.n3;
+  const int n_outer = ax2 ? d.n1 : d.n2;
+  const int outer_stride = ax2 ? d.n2 * d.n3 : d.n3;
+  const int nchunks = d.n3 / (2 * (NT / R2));
+  d2::strided_kernel<R2, FINAL, NT><<<dim3(n_outer * nchunks, ncomp), NT, sm, s>>>(
+      in, acc, add, out, d.n3, es, outer_stride, d.n(), ax2 ? p->tw2 : p->tw1, 1.0 / L, alpha);
+}
+
+template <int NT>
+static void spec_apply_A_d2_nt(vr_spec_plan* p, const float* in, int ncomp, double alpha, const float* add,
+                               float* out, float* acc, cudaStream_t s) {
+  const Dims& d = p->d;
+  if (d.n3 == 256) d2_rows<16, NT>(p, in, acc, ncomp, s); else d2_rows<8, NT>(p, in, acc, ncomp, s);
+  if (d.n2 == 256) d2_strided<16, false, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  else d2_strided<8, false, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  if (d.n1 == 256) d2_strided<16, true, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
+  else d2_strided<8, true, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
+}
+
+// out = alpha * (D33 + D22 + D11) in (+ add); the partial sums live in p->T
+static int spec_apply_A_d2(vr_spec_plan* p, const float* in, int ncomp, double alpha, const float* add, float* out,
+                           cudaStream_t s) {
+  float* acc = reinterpret_cast<float*>(p->T);   // 3 * nspec float2 >= 3 * N floats
+  if (g_d2_threads == 256) spec_apply_A_d2_nt<256>(p, in, ncomp, alpha, add, out, acc, s);
+  else spec_apply_A_d2_nt<128>(p, in, ncomp, alpha, add, out, acc, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
 extern "C" {
+
+int vr_set_spec_a_mode(int mode) {
+  // 0: 3-D f64 path; 1: separable engine (128-thread CTAs); 2: separable, 256-thread CTAs
+  const int prev = g_a_mode == 0 ? 0 : (g_d2_threads == 256 ? 2 : 1);
+  g_a_mode = mode != 0;
+  g_d2_threads = mode == 2 ? 256 : 128;
+  return prev;
+}
 
 // out = alpha * IFFT(symbol * FFT(in)) [+ add], component-wise or coupled (K).
 // alpha is folded into the f64 symbol (e.g. beta_v * A v + body in one call).
@@ -909,6 +989,7 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   if (kind == VR_SPEC_K && p->fast && xb(p->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
+  if (kind == VR_SPEC_A && d2_ok(p)) return spec_apply_A_d2(p, in, ncomp, alpha, add, out, s);
   const bool f64 = needs_f64(kind);
   int rc = spec_forward(p, in, ncomp, s, f64);
   if (rc) return rc;

@@ -147,6 +147,30 @@ def _device_axes(grid: Grid):
     return ax[0].view(-1, 1, 1), ax[1].view(1, -1, 1), ax[2].view(1, 1, -1)
 
 
+def velocity_tensor(K: int, grid: Grid, scale: float = 1.0) -> torch.Tensor:
+    """scale * make_velocity(K) evaluated on the device in f64 (the formulas of
+    velocity_array, synth.py:104-118) and rounded once to float32: for grids
+    whose host f64 lattice would not fit (1024^3: ~26 GB per array)."""
+    if K < 1:
+        raise ValueError("K must be >= 1")
+    x, y, z = _device_axes(grid)
+    xc, yc, zc = x - math.pi, y - math.pi, z - math.pi
+    out = torch.empty((3,) + tuple(grid.dims), dtype=torch.float32, device=x.device)
+    for c in range(3):
+        acc = torch.zeros(grid.dims, dtype=torch.float64, device=x.device)
+        for k in range(1, K + 1):
+            a = k ** -0.5
+            if c == 0:
+                acc += a * torch.cos(k * yc) * torch.cos(k * xc)
+            elif c == 1:
+                acc += a * torch.sin(k * zc) * torch.sin(k * yc)
+            else:
+                acc += a * torch.cos(k * xc) * torch.cos(k * zc)
+        out[c] = (scale * acc).to(torch.float32)
+        del acc
+    return out
+
+
 def c2_problem_device(grid: Grid, order: str = "cubic", n_t: int = 4):
     """c2_problem with the inputs evaluated on the device in f64 (same formulas
     as sphere_template / velocity_array, no host volume): for 1024^3 and up,
@@ -156,22 +180,7 @@ def c2_problem_device(grid: Grid, order: str = "cubic", n_t: int = 4):
     m0 = ScalarField(grid, (0.5 * (1.0 - torch.tanh((r - 1.2) / 0.19635))).to(torch.float32))
     lab0 = LabelMap(grid, (r <= 1.2).to(torch.int32))
     del r
-    xc, yc, zc = x - math.pi, y - math.pi, z - math.pi
-    comps = []
-    for c in range(3):
-        acc = torch.zeros(grid.dims, dtype=torch.float64, device=x.device)
-        for k in range(1, 3):
-            a = k ** -0.5
-            if c == 0:
-                acc += a * torch.cos(k * yc) * torch.cos(k * xc)
-            elif c == 1:
-                acc += a * torch.sin(k * zc) * torch.sin(k * yc)
-            else:
-                acc += a * torch.cos(k * xc) * torch.cos(k * zc)
-        comps.append((0.2 * acc).to(torch.float32))
-        del acc
-    vtrue = VectorField(grid, torch.stack(comps))
-    del comps
+    vtrue = VectorField(grid, velocity_tensor(2, grid, 0.2))
     cfg = TransportConfig(n_t, order)
     tops = TransportOperators(vtrue, cfg)
     m1 = solve_state(m0, vtrue, cfg, tops)
