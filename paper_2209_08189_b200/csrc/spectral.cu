@@ -504,6 +504,9 @@ static int g_fft_mode = 1;
 // A = |k|^2 through the separable f64 line engine (spectral_d2.cuh) where the
 // line lengths allow; vr_set_spec_a_mode(0) selects the 3-D f64 path.
 static int g_a_mode = 1;
+// x1 pass of component-diagonal symbols without the 3-component shared tile
+// (fs::xdiag256); vr_set_fft_mode(2) turns it off for A/B checks.
+static bool g_xdiag = true;
 
 using namespace vr;
 
@@ -635,8 +638,11 @@ bool needs_f64(int kind) { return kind == VR_SPEC_A || kind == VR_SPEC_A2; }
 extern "C" {
 
 int vr_set_fft_mode(int mode) {
-  const int prev = g_fft_mode;
-  g_fft_mode = mode;
+  // 0: Stockham only; 1 (default): four-step kernels incl. the diagonal x1 pass;
+  // 2: four-step kernels with the 3-component x1 tile for every symbol
+  const int prev = g_fft_mode == 0 ? 0 : (g_xdiag ? 1 : 2);
+  g_fft_mode = mode != 0;
+  g_xdiag = mode == 1;
   return prev;
 }
 
@@ -853,6 +859,21 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
     for (int c = 0; c < 3; ++c)
       nblk = spec_xpass(p, o1, false, s, f64, reinterpret_cast<const char*>(Sd) + c * cstride * esz, Tt + c * cstride);
     return nblk;
+  }
+  if (p->fast && g_fft_mode && d.n1 == 256 && !reduce && op.kind != VR_SPEC_K && g_xdiag) {
+    // component-diagonal symbol: one component per CTA row, no shared tile
+    const int nchunks = (p->n3h + 15) / 16;
+    const dim3 g(d.n2 * nchunks, nc);
+    if (f64) {
+      const size_t sm = sizeof(double2) * 16 * fs::line_smem<16>();
+      smem_optin(fs::xdiag256<double2>, sm);
+      fs::xdiag256<double2><<<g, 256, sm, s>>>(Sd, Tt, d.n2, p->n3h, p->tw1, op);
+    } else {
+      const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
+      smem_optin(fs::xdiag256<float2>, sm);
+      fs::xdiag256<float2><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(Sd), Tt, d.n2, p->n3h, p->tw1, op);
+    }
+    return g.x;
   }
   if (p->fast && g_fft_mode && d.n1 == 256 && nc == 3 && !reduce) {
     constexpr int LS = 273;

@@ -215,5 +215,59 @@ __global__ void __launch_bounds__(3 * XB * 16, (sizeof(CF) == 8 ? 20 : 12) / XB)
   }
 }
 
+// ---- X pass for component-DIAGONAL symbols (A, shifted inverses, Gaussian),
+// L = n1 = 256: one component per CTA row of the grid, NB = 16 consecutive kz
+// per CTA (lane = q + NB t: every warp access is a 128-B contiguous run of
+// float2, 256 B of double2), forward (CF) -> symbol in registers -> inverse
+// (f32) -> T.  No shared tile: a line's spectrum never leaves its 16 threads
+// (the symbol of a diagonal operator needs no other component), so the pass
+// costs the two line FFTs' transposes only.  grid (n2 * nchunks, ncomp).
+template <int R2>
+__device__ __forceinline__ void diag_symbol_at(const SpecOp& op, int k1, double k2, double k3, double2& v) {
+  double2 vals[1] = {v};
+  SpecOp o1 = op;
+  o1.ncomp = 1;
+  apply_symbol(o1, (double)k1, k2, k3, vals);
+  v = vals[0];
+}
+
+template <typename CF>
+__global__ void __launch_bounds__(256, sizeof(CF) == 8 ? 3 : 2) xdiag256(const CF* __restrict__ S,
+                                                                      float2* __restrict__ T, int n2, int n3h,
+                                                                      const double2* __restrict__ tw, SpecOp op) {
+  constexpr int R2 = 16, NB = 16, L = 256;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int q = threadIdx.x % NB, t = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB;
+  const int c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
+  const int64_t lstride = (int64_t)n2 * n3h;
+  const CF* sb = S + (int64_t)j * n3h + kz0 + q;
+  CF v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (ok) v[m] = sb[op.xoff(c, t + R2 * m, lstride)];
+    else { v[m].x = 0; v[m].y = 0; }
+  }
+  CF* sm = reinterpret_cast<CF*>(fs_smem) + q * line_smem<R2>();
+  line_fft<CF, R2>(v, t, sm, tw, false);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)(kz0 + q);
+  float2 w[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    double2 a = to_d(v[u]);
+    diag_symbol_at<R2>(op, signed_freq(out_freq<R2>(t, u), L), k2, k3, a);
+    w[u] = make_float2((float)a.x, (float)a.y);
+  }
+  __syncthreads();   // transpose scratch reused by the inverse
+  line_fft<float2, R2>(w, t, reinterpret_cast<float2*>(fs_smem) + q * line_smem<R2>(), tw, true);
+  if (ok) {
+    float2* tb = T + (int64_t)j * n3h + kz0 + q;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tb[op.xoff(c, out_freq<R2>(t, u), lstride)] = w[u];
+  }
+}
+
 }  // namespace fs
 }  // namespace vr

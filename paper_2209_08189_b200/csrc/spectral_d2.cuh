@@ -11,9 +11,10 @@
 //     A 3-D f32 transform cannot meet the 1e-5 operator bar at 256^3 (SURVEY §7:
 //     3-5e-5), which is why the 3-D path stores its forward half in f64 (2.8 GB
 //     of pass traffic per A at 256^3).  Here a line is loaded from the f32
-//     field, transformed, multiplied and transformed back entirely in f64
-//     REGISTERS; the only roundings are the three f32 partial sums, relative
-//     to the output (~1e-7).
+//     field and forward-transformed and multiplied in f64 registers; the
+//     inverse runs in f32 (its rounding is relative to the output), and the
+//     three partial sums are f32 -- every rounding after the multiply is
+//     relative to |A v| (~1e-7).
 //   * Traffic: three passes (x3, x2, x1), each reading v once and the running
 //     partial sum, 32-36 B/voxel per component instead of ~55 B (3-D, f64).
 // Two real lines travel as one complex line (a + i b): the symbol is real and
@@ -36,10 +37,10 @@ namespace d2 {
 
 // input slot of the forward line FFT for the value thread t holds at output
 // position u (see fs::out_freq): identity for R2 = 16, interleave for R2 = 8
-template <int R2>
-__device__ __forceinline__ void to_input_order(double2 (&v)[16]) {
+template <int R2, typename C>
+__device__ __forceinline__ void to_input_order(C (&v)[16]) {
   if constexpr (R2 == 8) {
-    double2 w[16];
+    C w[16];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       w[2 * u] = v[u];
@@ -50,11 +51,13 @@ __device__ __forceinline__ void to_input_order(double2 (&v)[16]) {
   }
 }
 
-// forward line FFT -> multiply by scale * k^2 (k = fftfreq * L) -> inverse.
-// Values enter as x[t + R2 m] and leave as y[out_freq(t, u)].
+// forward line FFT (f64) -> multiply by scale * k^2 (k = fftfreq * L) ->
+// inverse (f32: after the multiply every value is O(|D x|), so the inverse's
+// rounding is relative to the output, as in the 3-D engine's inverse half).
+// Values enter as x[t + R2 m] (f64) and leave as y[out_freq(t, u)] (f32).
 template <int R2>
-__device__ __forceinline__ void line_d2(double2 (&v)[16], int t, double2* sm, const double2* __restrict__ tw,
-                                        double scale) {
+__device__ __forceinline__ void line_d2(double2 (&v)[16], float2 (&y)[16], int t, double2* sm,
+                                        const double2* __restrict__ tw, double scale) {
   constexpr int L = 16 * R2;
   fs::line_fft<double2, R2>(v, t, sm, tw, false);
 #pragma unroll
@@ -62,12 +65,11 @@ __device__ __forceinline__ void line_d2(double2 (&v)[16], int t, double2* sm, co
     const int k = fs::out_freq<R2>(t, u);
     const double f = (double)(k < L / 2 ? k : k - L);
     const double m = f * f * scale;
-    v[u].x *= m;
-    v[u].y *= m;
+    y[u] = make_float2((float)(v[u].x * m), (float)(v[u].y * m));
   }
-  to_input_order<R2>(v);
+  to_input_order<R2>(y);
   __syncthreads();   // the transpose scratch is reused by the inverse
-  fs::line_fft<double2, R2>(v, t, sm, tw, true);
+  fs::line_fft<float2, R2>(y, t, reinterpret_cast<float2*>(sm), tw, true);
 }
 
 // x3 lines: one complex line = rows (2p, 2p+1) of the flattened (n1 n2, n3)
@@ -87,15 +89,16 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) rows_kernel(const float
   double2 x[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) x[m] = make_double2(__ldg(ra + t + R2 * m), __ldg(rb + t + R2 * m));
-  line_d2<R2>(x, t, smem + q * fs::line_smem<R2>(), tw, scale);
+  float2 y[16];
+  line_d2<R2>(x, y, t, smem + q * fs::line_smem<R2>(), tw, scale);
   if (ok) {
     float* wa = acc + blockIdx.y * cstride + (int64_t)p * 2 * L;
     float* wb = wa + L;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int k = fs::out_freq<R2>(t, u);
-      wa[k] = (float)x[u].x;
-      wb[k] = (float)x[u].y;
+      wa[k] = y[u].x;
+      wb[k] = y[u].y;
     }
   }
 }
@@ -126,7 +129,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) strided_kernel(const fl
     const float2 a = __ldg(vb + ((base + (t + R2 * m) * es) >> 1));
     x[m] = make_double2(a.x, a.y);
   }
-  line_d2<R2>(x, t, smem + q * fs::line_smem<R2>(), tw, scale);
+  float2 y[16];
+  line_d2<R2>(x, y, t, smem + q * fs::line_smem<R2>(), tw, scale);
   float2* ab = reinterpret_cast<float2*>(acc + cb);
   float2* ob = reinterpret_cast<float2*>(out + cb);
   const float2* db = add ? reinterpret_cast<const float2*>(add + cb) : nullptr;
@@ -136,8 +140,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) strided_kernel(const fl
     const float2 s = ab[e];
     float2 r;
     if (FINAL) {
-      r.x = (float)(alpha * ((double)s.x + x[u].x));
-      r.y = (float)(alpha * ((double)s.y + x[u].y));
+      r.x = (float)(alpha * ((double)s.x + (double)y[u].x));
+      r.y = (float)(alpha * ((double)s.y + (double)y[u].y));
       if (db) {
         const float2 b = __ldg(db + e);
         r.x += b.x;
@@ -145,8 +149,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) strided_kernel(const fl
       }
       ob[e] = r;
     } else {
-      r.x = (float)((double)s.x + x[u].x);
-      r.y = (float)((double)s.y + x[u].y);
+      r.x = s.x + y[u].x;
+      r.y = s.y + y[u].y;
       ab[e] = r;
     }
   }

@@ -197,29 +197,49 @@ def test_1024_fd8_sampled_bit_exact(P, c3):
 
 def test_1024_spectral_vs_cufft_f64(P, c3):
     """A, shifted inverse and K at 1024^3 against torch.fft (cuFFT) in float64
-    on the identical float32 input (test-only cross-check)."""
-    import sys
-    import os
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    from spec_probe import cufft_op
+    on the identical float32 input (test-only cross-check), one f64 component
+    at a time (a 1024^3 complex128 half spectrum is 8.6 GB)."""
     g, v = c3["g"], c3["v"]
     ops = P.RegOperators.for_grid(g, 1e-2, 1e-4)
     V = P.VectorField(g, v)
+    dims = tuple(g.dims)
+    n1, n2, n3 = dims
+    dev = v.device
+    k1 = torch.fft.fftfreq(n1, d=1.0 / n1, dtype=torch.float64, device=dev).view(n1, 1, 1)
+    k2 = torch.fft.fftfreq(n2, d=1.0 / n2, dtype=torch.float64, device=dev).view(1, n2, 1)
+    k3 = torch.arange(n3 // 2 + 1, dtype=torch.float64, device=dev).view(1, 1, -1)
+    ksq = k1 ** 2 + k2 ** 2 + k3 ** 2
+    ks = (k1, k2, k3)
 
-    def err(got, ref):
-        return float(torch.linalg.vector_norm((got.double() - ref).flatten()) / torch.linalg.vector_norm(ref.flatten()))
+    def rfft(c):
+        return torch.fft.rfftn(v[c].double())
 
-    for name, fn in (("A", lambda: P.apply_A(V, ops).data),
-                     ("invshift", lambda: P.apply_inv_shifted_A(V, ops, 1.0).data),
-                     ("K", lambda: P.apply_K(V, ops).data)):
-        got = fn()
-        ref = torch.empty((3,) + tuple(g.dims), dtype=torch.float64, device="cuda")
-        if name == "K":
-            ref = cufft_op("K", v)
-        else:
-            for c in range(3):   # one component at a time (8.6 GB f64 spectra)
-                ref[c] = cufft_op(name, v[c:c + 1])[0]
-        e = err(got, ref)
-        del ref, got
-        torch.cuda.empty_cache()
-        assert e < TOL, (name, e)
+    def irfft(F):
+        return torch.fft.irfftn(F, s=dims)
+
+    def check(got, refs):
+        num = den = 0.0
+        for c in range(3):
+            r = refs(c)
+            num += float(torch.sum((got[c].double() - r) ** 2))
+            den += float(torch.sum(r ** 2))
+            del r
+        return math.sqrt(num / den)
+
+    got = P.apply_A(V, ops).data
+    assert check(got, lambda c: irfft(rfft(c) * ksq)) < TOL
+    got = P.apply_inv_shifted_A(V, ops, 1.0).data
+    assert check(got, lambda c: irfft(rfft(c) / (1e-2 * ksq + 1.0))) < TOL
+    got = P.apply_K(V, ops).data
+    cb = 1e-4 * (1 + ksq) / (1e-2 * ksq + 1e-4 * (1 + ksq))
+    f = torch.where(ksq > 0, cb / torch.where(ksq > 0, ksq, torch.ones_like(ksq)), torch.zeros_like(ksq))
+    kd = None
+    for c in range(3):
+        t = ks[c] * rfft(c)
+        kd = t if kd is None else kd + t
+        del t
+    kd *= f
+    del f, cb
+    assert check(got, lambda c: irfft(rfft(c) - ks[c] * kd)) < TOL
+    del kd, got
+    torch.cuda.empty_cache()
