@@ -90,6 +90,17 @@ int vr_set_fft_mode(int mode);
  * with an f64 forward half.  Returns the previous mode. */
 int vr_set_spec_a_mode(int mode);
 
+/* Tuning switches of the spectral engine (no reference counterpart; results
+ * agree to rounding).  key 1: run component-diagonal symbols (A, shifted
+ * inverses, Gaussian) on 3-component fields one component at a time (value 1,
+ * default) or all components per pass (0).  Returns the previous value, or
+ * VR_ERR_ARG for an unknown key. */
+int vr_set_spectral_tuning(int key, int value);
+
+/* Number of kernel launches one vr_spec_apply(p, kind, ., ncomp, ...) makes
+ * with the current tuning (launch accounting for benchmarks). */
+int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp);
+
 /* Tuning switch (no reference counterpart) for the single-domain RK2 trace:
  * 0 (default) = general flat-index gathers, 1 = lean periodic gathers on a 3-D
  * launch (measured slower: 3.83 vs 2.41 ms at C2 cubic).  Same taps; summation

@@ -37,6 +37,8 @@ _SIGS = {
     "vr_set_gather_mode": [_i32],
     "vr_set_fft_mode": [_i32],
     "vr_set_spec_a_mode": [_i32],
+    "vr_set_spectral_tuning": [_i32, _i32],
+    "vr_spec_apply_launches": [_p, _i32, _i32],
     "vr_set_trace_mode": [_i32],
     "vr_advect": [_p, _dims_t, _p, _p, _i32, _p, _p, _p],
     "vr_incstate_init": [_p, _p, _dims_t, _f64, _p, _p],
@@ -90,7 +92,7 @@ class NativeError(VelregError):
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches accounting)
-LAUNCHES = {"vr_spec_apply": 5, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
+LAUNCHES = {"vr_spec_apply_launches": 0, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
             "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
@@ -150,20 +152,30 @@ class timed:
         return False
 
 
+fn_launches = None
+
+
 class _Bound:
     def __init__(self, lib):
         self._raw = lib
+        global fn_launches
+        fn_launches = lib.vr_spec_apply_launches
         for name in _SIGS:
             setattr(self, name, self._wrap(name, getattr(lib, name)))
 
     @staticmethod
     def _wrap(name, fn):
         n_launch = LAUNCHES.get(name, 1)
+        count_fn = None
+        if name == "vr_spec_apply":   # depends on the operator, the plan and the tuning
+            def count_fn(args):
+                return int(fn_launches(args[0], args[1], args[3]))
 
         def call(*args):
             prof = PROFILE
             if not prof.enabled:
                 return fn(*args)
+            n = count_fn(args) if count_fn else n_launch
             if name in prof.timed:
                 s = torch.cuda.current_stream()
                 a = torch.cuda.Event(enable_timing=True)
@@ -174,7 +186,7 @@ class _Bound:
                 prof.events[name].append((a, b))
             else:
                 rc = fn(*args)
-            prof.launches[name] = prof.launches.get(name, 0) + n_launch
+            prof.launches[name] = prof.launches.get(name, 0) + n
             return rc
 
         call.__name__ = name

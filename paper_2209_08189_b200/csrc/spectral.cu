@@ -507,6 +507,8 @@ static int g_a_mode = 1;
 // x1 pass of component-diagonal symbols without the 3-component shared tile
 // (fs::xdiag256); vr_set_fft_mode(2) turns it off for A/B checks.
 static bool g_xdiag = true;
+// diagonal symbols on 3-component fields: one component at a time (L2 reuse)
+static int g_percomp = 1;
 
 using namespace vr;
 
@@ -993,6 +995,26 @@ static int spec_apply_A_d2(vr_spec_plan* p, const float* in, int ncomp, double a
 
 extern "C" {
 
+// kernel launches one vr_spec_apply(p, kind, ., ncomp, ...) makes (bench accounting)
+int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp) {
+  if (!p) return 0;
+  if (kind == VR_SPEC_A && d2_ok(p)) return 3;
+  const bool x3split = p->fast && ncomp == 3 && xb(p->d.n1, 3) == 0 && !(g_fft_mode && p->d.n1 == 256);
+  const int per = 5 + (x3split ? 2 : 0);
+  if (ncomp == 3 && kind != VR_SPEC_K && g_percomp) return 15;
+  return per;
+}
+
+int vr_set_spectral_tuning(int key, int value) {
+  // key 1: per-component scheduling of diagonal symbols (1 = on, 0 = all components per pass)
+  if (key == 1) {
+    const int prev = g_percomp;
+    g_percomp = value;
+    return prev;
+  }
+  return VR_ERR_ARG;
+}
+
 int vr_set_spec_a_mode(int mode) {
   // 0: 3-D f64 path; 1: separable engine (128-thread CTAs); 2: separable, 256-thread CTAs
   const int prev = g_a_mode == 0 ? 0 : (g_d2_threads == 256 ? 2 : 1);
@@ -1012,6 +1034,21 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   const Dims& d = p->d;
   if (kind == VR_SPEC_A && d2_ok(p)) return spec_apply_A_d2(p, in, ncomp, alpha, add, out, s);
   const bool f64 = needs_f64(kind);
+  if (ncomp == 3 && kind != VR_SPEC_K && g_percomp) {
+    // component-diagonal symbol: run the five passes one component at a time
+    // on the same spectrum buffer, so a component's half spectrum (67.6 MB in
+    // f32 at 256^3) is still in L2 when the next pass reads it
+    const int64_t n = d.n();
+    SpecOp op{kind, 1, beta_v, beta_w, shift, alpha / (double)n, sigma, 0, d.n2, d.n1};
+    for (int c = 0; c < 3; ++c) {
+      int rc = spec_forward(p, in + c * n, 1, s, f64);
+      if (rc) return rc;
+      spec_xpass(p, op, false, s, f64);
+      spec_inverse_yz(p, 1, add ? add + c * n : nullptr, out + c * n, s);
+    }
+    VR_CHECK_LAUNCH();
+    return VR_OK;
+  }
   int rc = spec_forward(p, in, ncomp, s, f64);
   if (rc) return rc;
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)d.n(), sigma, 0, d.n2, d.n1};

@@ -92,10 +92,14 @@ def main():
         for name, (kind, kw) in kinds.items():
             for fname, v in (("c2_velocity", v_real), ("velocity_plus_noise", v_noise)):
                 ref = cufft_op(name, v)
-                modes = [("engine", None)]
+                modes = [("engine_percomp", (None, 1)), ("engine_allcomp", (None, 0))]
                 if name == "A":
-                    modes = [("separable_f64_128t", 1), ("separable_f64_256t", 2), ("3d_f64_forward", 0)]
-                for mname, mode in modes:
+                    modes = [("separable_f64_128t", (1, 1)), ("separable_f64_256t", (2, 1)),
+                             ("3d_f64_forward_percomp", (0, 1)), ("3d_f64_forward_allcomp", (0, 0))]
+                if name == "K":
+                    modes = [("engine", (None, 1))]
+                for mname, (mode, pc) in modes:
+                    lib.vr_set_spectral_tuning(1, pc)
                     if mode is not None:
                         lib.vr_set_spec_a_mode(mode)
                     out = ws.apply(kind, v, **kw)
@@ -106,6 +110,7 @@ def main():
                                 "ms": t, "gbs_24B": 24 * n ** 3 / (t * 1e-3) / 1e9})
                     print(json.dumps(res[-1]), flush=True)
                 lib.vr_set_spec_a_mode(1)
+                lib.vr_set_spectral_tuning(1, 1)
                 for dt, dname in ((torch.float32, "cufft_f32"), (torch.float64, "cufft_f64")):
                     if fname != "c2_velocity":
                         continue
