@@ -507,8 +507,11 @@ static int g_a_mode = 1;
 // x1 pass of component-diagonal symbols without the 3-component shared tile
 // (fs::xdiag256); vr_set_fft_mode(2) turns it off for A/B checks.
 static bool g_xdiag = true;
-// diagonal symbols on 3-component fields: one component at a time (L2 reuse)
-static int g_percomp = 1;
+// diagonal symbols on 3-component fields: one component at a time (L2 reuse of
+// the half spectrum).  Measured slower on B200 at 256^3 (shifted inverse 0.714
+// vs 0.656 ms, A 3-D 0.898 vs 0.841 ms: three times the launches and tails for
+// no DRAM saving), so off by default; kept as an A/B switch.
+static int g_percomp = 0;
 
 using namespace vr;
 
