@@ -40,6 +40,7 @@ _SIGS = {
     "vr_set_spectral_tuning": [_i32, _i32],
     "vr_spec_apply_launches": [_p, _i32, _i32],
     "vr_set_trace_mode": [_i32],
+    "vr_set_fd8_mode": [_i32],
     "vr_advect": [_p, _dims_t, _p, _p, _i32, _p, _p, _p],
     "vr_incstate_init": [_p, _p, _dims_t, _f64, _p, _p],
     "vr_incstate_step": [_p, _dims_t, _p, _p, _p, _f64, _i32, _i32, _p, _p, _p],

@@ -391,6 +391,277 @@ void fd8_run(dim3 block, cudaStream_t s, const float* in, const float* lo, const
                                                      nchunk);
 }
 
+// ---- row-tile FD8 with bulk-copy plane staging (N3 in {128, 256, 512}) -------
+// One CTA = TY whole x2 rows (every x3 voxel) walked along a chunk of x1
+// planes.  Each plane step is staged in shared memory by ONE bulk copy per
+// row (cp.async.bulk, 0.5-2 KB contiguous, completion on an mbarrier): the
+// x2-halo'd rows of plane p (x2 / x3 derivatives) and the TY centre rows of
+// plane p + 4 (the leading edge of the x1 register windows), NS plane steps in
+// flight.  A row tile spans the whole x3 extent, so the x3 stencil wraps
+// inside the staged row and only the x2 halo rows ever wrap (done by the
+// producer's row addresses).  Thread = 4 consecutive x3 voxels (float4) x RY
+// rows; arithmetic and division exactly as fd8_kernel (bit-identical).
+// MODE 0: gradient of f; MODE 1: divergence of v (v2 halo'd rows, v3 and the
+// plane-ahead v1 centre rows).
+template <int N3> struct RowCfg;
+template <> struct RowCfg<128> { static constexpr int TPR = 32, RPP = 8, RY = 1, TY = 8, NS = 4; };
+template <> struct RowCfg<256> { static constexpr int TPR = 64, RPP = 4, RY = 2, TY = 8, NS = 4; };
+template <> struct RowCfg<512> { static constexpr int TPR = 128, RPP = 2, RY = 2, TY = 4, NS = 3; };
+
+template <int MODE, int N3> struct RowStage {
+  using C = RowCfg<N3>;
+  // row blocks: [0, TY+8) x2-halo'd rows (f or v2); then TY centre rows of the
+  // plane 4 ahead (f or v1); MODE 1 adds TY centre rows of v3
+  static constexpr int ROWS = C::TY + 8 + C::TY + (MODE == 1 ? C::TY : 0);
+  static constexpr int HALO_ROW = 0, XC_ROW = C::TY + 8, Z_ROW = 2 * C::TY + 8;
+  static constexpr size_t BYTES = sizeof(float) * ROWS * N3;
+};
+
+__device__ __forceinline__ unsigned fd8_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int MODE, bool SLAB, int N3>
+__global__ void __launch_bounds__(256, 2) fd8_rows_kernel(const float* __restrict__ f, const float* __restrict__ lo,
+                                                          const float* __restrict__ hi, Dims d, float h1, float h2,
+                                                          float h3, float r1, float r2, float r3, unsigned dlo,
+                                                          unsigned dspan, float* __restrict__ out, int nchunk) {
+  using C = RowCfg<N3>;
+  using St = RowStage<MODE, N3>;
+  constexpr int TY = C::TY, RY = C::RY, RPP = C::RPP, NS = C::NS, TPR = C::TPR;
+  extern __shared__ __align__(128) float rows_smem[];
+  __shared__ __align__(8) unsigned long long full[NS];
+  const int64_t N = d.n();
+  const int psz = d.n2 * N3;
+  const int ntiles = d.n2 / TY;
+  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int i_begin = (int)((int64_t)d.n1 * chunk / nchunk);
+  const int i_end = (int)((int64_t)d.n1 * (chunk + 1) / nchunk);
+  const int j0 = tile * TY;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int tc = tid % TPR, ty = tid / TPR;      // float4 column, first tile row of the thread
+  const int k = 4 * tc;
+  if (tid < NS) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fd8_smem_u32(&full[tid])) : "memory");
+  }
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (i_begin >= i_end) return;
+
+  auto plane = [&](const float* base, int ii) -> const float* {   // plane ii in [-4, L1 + 4)
+    if (SLAB) return ii < 0 ? lo + (int64_t)(ii + HALO) * psz
+                            : (ii >= d.n1 ? hi + (int64_t)(ii - d.n1) * psz : base + (int64_t)ii * psz);
+    ii = ii < 0 ? ii + d.n1 : (ii >= d.n1 ? ii - d.n1 : ii);
+    return base + (int64_t)ii * psz;
+  };
+  // component bases: MODE 0 f; MODE 1 v1 = f, v2 = f + N, v3 = f + 2N (ghosts only for v1)
+  const float* fx = f;                              // x1 windows
+  const float* fy = MODE == 0 ? f : f + N;          // x2 halo'd rows
+  // producer: warp 0, one bulk copy per staged row
+  auto issue = [&](int p) {
+    if (tid >= 32) return;
+    const int s = p % NS;
+    float* st = rows_smem + (size_t)s * St::ROWS * N3;
+    const unsigned bar = fd8_smem_u32(&full[s]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)St::BYTES)
+                   : "memory");
+    __syncwarp();
+    for (int r = lane; r < St::ROWS; r += 32) {
+      const float* src;
+      if (r < TY + 8) {                       // x2-halo'd rows of plane p (x1 local: never a ghost for x2/x3)
+        int jr = j0 - HALO + r;
+        jr = jr < 0 ? jr + d.n2 : (jr >= d.n2 ? jr - d.n2 : jr);
+        src = fy + (int64_t)p * psz + (int64_t)jr * N3;
+      } else if (r < 2 * TY + 8) {            // centre rows of plane p + 4 (x1 window, may be a ghost)
+        src = plane(fx, p + HALO) + (int64_t)(j0 + r - (TY + 8)) * N3;
+      } else {                                // MODE 1: centre rows of v3, plane p
+        src = f + 2 * N + (int64_t)p * psz + (int64_t)(j0 + r - (2 * TY + 8)) * N3;
+      }
+      const unsigned dst = fd8_smem_u32(st + (size_t)r * N3);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"((unsigned)(N3 * 4)), "r"(bar) : "memory");
+    }
+  };
+
+  // x1 windows: plane i-4+o of row r, column c in w[r][c][(S + o) % 9]
+  float w[RY][4][9];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    const float* pl = plane(fx, i_begin - HALO + o);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(pl + (int64_t)(j0 + ty + r * RPP) * N3 + k));
+      w[r][0][o] = v.x; w[r][1][o] = v.y; w[r][2][o] = v.z; w[r][3][o] = v.w;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q)
+    if (i_begin + q < i_end) issue(i_begin + q);
+
+  auto step = [&](auto S_, int i) {
+    constexpr int S = decltype(S_)::value;
+    const int s = i % NS;
+    if (i + NS - 1 < i_end) issue(i + NS - 1);   // stage (i - 1) % NS: released by the barrier below
+    {
+      const unsigned bar = fd8_smem_u32(&full[s]);
+      const unsigned par = (unsigned)((i - i_begin) / NS) & 1u;
+      asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\t"
+                   "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}"
+                   ::"r"(bar), "r"(par) : "memory");
+    }
+    const float* st = rows_smem + (size_t)s * St::ROWS * N3;
+    // window leading edge (plane i + 4)
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(st + (size_t)(St::XC_ROW + ty + r * RPP) * N3 + k);
+      w[r][0][(S + 8) % 9] = v.x; w[r][1][(S + 8) % 9] = v.y;
+      w[r][2][(S + 8) % 9] = v.z; w[r][3][(S + 8) % 9] = v.w;
+    }
+    float g1[RY][4], g2[RY][4], g3[RY][4];
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float* x = w[r][c];
+        g1[r][c] = fd8_sum(x[(S + 5) % 9], x[(S + 6) % 9], x[(S + 7) % 9], x[(S + 8) % 9], x[(S + 3) % 9],
+                           x[(S + 2) % 9], x[(S + 1) % 9], x[S % 9]);
+      }
+    // x2: halo'd rows ty + r RPP - 4 .. + 4 (staged row index = tile row + 4)
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      float Y[9][4];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        if (q == 4) continue;
+        const float4 v = *reinterpret_cast<const float4*>(st + (size_t)(ty + r * RPP + q) * N3 + k);
+        Y[q][0] = v.x; Y[q][1] = v.y; Y[q][2] = v.z; Y[q][3] = v.w;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        g2[r][c] = fd8_sum(Y[5][c], Y[6][c], Y[7][c], Y[8][c], Y[3][c], Y[2][c], Y[1][c], Y[0][c]);
+    }
+    // x3: columns k-4 .. k+7 of the row, wrapped inside the staged row
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const float* row = MODE == 0 ? st + (size_t)(ty + r * RPP + HALO) * N3
+                                   : st + (size_t)(St::Z_ROW + ty + r * RPP) * N3;
+      const int km = k == 0 ? N3 - 4 : k - 4, kp = k + 4 == N3 ? 0 : k + 4;
+      const float4 a = *reinterpret_cast<const float4*>(row + km);
+      const float4 b = *reinterpret_cast<const float4*>(row + k);
+      const float4 e = *reinterpret_cast<const float4*>(row + kp);
+      const float Z[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int m = c + HALO;
+        g3[r][c] = fd8_sum(Z[m + 1], Z[m + 2], Z[m + 3], Z[m + 4], Z[m - 1], Z[m - 2], Z[m - 3], Z[m - 4]);
+      }
+    }
+    __syncthreads();   // every reader of stage s is done: the next issue() may refill it
+    bool ieee = false;
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
+                div_needs_ieee(g3[r][c], dlo, dspan);
+    if (ieee) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        F12 sv;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          sv.v[c] = g1[r][c];
+          sv.v[4 + c] = g2[r][c];
+          sv.v[8 + c] = g3[r][c];
+        }
+        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g1[r][c] = sv.v[c];
+          g2[r][c] = sv.v[4 + c];
+          g3[r][c] = sv.v[8 + c];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g1[r][c] = div_fast(g1[r][c], h1, r1);
+          g2[r][c] = div_fast(g2[r][c], h2, r2);
+          g3[r][c] = div_fast(g3[r][c], h3, r3);
+        }
+    }
+    float* op = out + (int64_t)i * psz;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      float4* o = reinterpret_cast<float4*>(op + (int64_t)(j0 + ty + r * RPP) * N3 + k);
+      if constexpr (MODE == 0) {
+        o[0] = make_float4(g1[r][0], g1[r][1], g1[r][2], g1[r][3]);
+        o[N / 4] = make_float4(g2[r][0], g2[r][1], g2[r][2], g2[r][3]);
+        o[N / 2] = make_float4(g3[r][0], g3[r][1], g3[r][2], g3[r][3]);
+      } else {
+        float4 q;
+        q.x = __fadd_rn(__fadd_rn(g1[r][0], g2[r][0]), g3[r][0]);
+        q.y = __fadd_rn(__fadd_rn(g1[r][1], g2[r][1]), g3[r][1]);
+        q.z = __fadd_rn(__fadd_rn(g1[r][2], g2[r][2]), g3[r][2]);
+        q.w = __fadd_rn(__fadd_rn(g1[r][3], g2[r][3]), g3[r][3]);
+        o[0] = q;
+      }
+    }
+  };
+#define VR_FD8R_STEP(S)        \
+  if (i >= i_end) break;       \
+  step(IC<S>{}, i);            \
+  ++i;
+  for (int i = i_begin;;) {
+    VR_FD8R_STEP(0) VR_FD8R_STEP(1) VR_FD8R_STEP(2) VR_FD8R_STEP(3) VR_FD8R_STEP(4)
+    VR_FD8R_STEP(5) VR_FD8R_STEP(6) VR_FD8R_STEP(7) VR_FD8R_STEP(8)
+  }
+#undef VR_FD8R_STEP
+}
+
+template <int MODE, bool SLAB, int N3>
+void fd8_rows_run(cudaStream_t s, const float* in, const float* lo, const float* hi, Dims d, float h1, float h2,
+                  float h3, float r1, float r2, float r3, unsigned dlo, unsigned dspan, float* out) {
+  using C = RowCfg<N3>;
+  const size_t smem = RowStage<MODE, N3>::BYTES * C::NS;
+  static int slots = 0;   // resident CTAs per GPU (per instantiation)
+  if (!slots) {
+    cudaFuncSetAttribute(fd8_rows_kernel<MODE, SLAB, N3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fd8_rows_kernel<MODE, SLAB, N3>, 256, smem);
+    slots = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int ntiles = d.n2 / C::TY;
+  // ~2 waves of CTAs, chunks of >= 8 planes (the 8-plane window preload is amortised)
+  const int nchunk = std::max(1, std::min((2 * slots + ntiles - 1) / ntiles, d.n1 / 8));
+  fd8_rows_kernel<MODE, SLAB, N3><<<ntiles * nchunk, 256, smem, s>>>(in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo,
+                                                                    dspan, out, nchunk);
+}
+
+// 0: cp.async tile kernel only; 1 (default): row-tile bulk-copy kernel where it applies
+static int g_fd8_mode = 1;
+
+template <int MODE, bool SLAB>
+bool fd8_rows_dispatch(cudaStream_t s, const float* in, const float* lo, const float* hi, Dims d, float h1,
+                       float h2, float h3, float r1, float r2, float r3, unsigned dlo, unsigned dspan, float* out) {
+  if (!g_fd8_mode || (((uintptr_t)in | (uintptr_t)out | (uintptr_t)lo | (uintptr_t)hi) & 15)) return false;
+  if (d.n1 < 8) return false;
+  switch (d.n3) {
+    case 128: if (d.n2 % RowCfg<128>::TY) return false;
+      fd8_rows_run<MODE, SLAB, 128>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
+    case 256: if (d.n2 % RowCfg<256>::TY) return false;
+      fd8_rows_run<MODE, SLAB, 256>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
+    case 512: if (d.n2 % RowCfg<512>::TY) return false;
+      fd8_rows_run<MODE, SLAB, 512>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
+    default: return false;
+  }
+}
+
 }  // namespace vr
 
 using namespace vr;
@@ -416,6 +687,15 @@ static int fd8_launch(int mode, const float* in, const float* lo, const float* h
   const unsigned dspan = (verified ? 0x79800000u : 0x5d800000u) - dlo;  // 2^116 / 2^60
   dim3 block(TXB, TYB);
   cudaStream_t s = (cudaStream_t)stream;
+  bool done;
+  if (mode == 0 && slab) done = fd8_rows_dispatch<0, true>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out);
+  else if (mode == 0) done = fd8_rows_dispatch<0, false>(s, in, nullptr, nullptr, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out);
+  else if (slab) done = fd8_rows_dispatch<1, true>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out);
+  else done = fd8_rows_dispatch<1, false>(s, in, nullptr, nullptr, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out);
+  if (done) {
+    VR_CHECK_LAUNCH();
+    return VR_OK;
+  }
   if (mode == 0 && slab)
     fd8_run<0, true>(block, s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out);
   else if (mode == 0)
@@ -429,6 +709,11 @@ static int fd8_launch(int mode, const float* in, const float* lo, const float* h
 }
 
 extern "C" {
+int vr_set_fd8_mode(int mode) {
+  const int prev = g_fd8_mode;
+  g_fd8_mode = mode;
+  return prev;
+}
 int vr_fd8_grad(const float* f, const int64_t dims[3], float* out3, void* stream) {
   return fd8_launch(0, f, nullptr, nullptr, dims, dims ? dims[0] : 0, out3, stream);
 }

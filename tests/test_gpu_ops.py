@@ -66,7 +66,8 @@ def test_fd8_bit_exact(P, ops_fx):
     assert rel_l2(got, ops_fx["fd8_div"]) < TOL
 
 
-@pytest.mark.parametrize("dims", [(10, 14, 10), (40, 72, 96), (64, 64, 64)])
+@pytest.mark.parametrize("dims", [(10, 14, 10), (40, 72, 96), (64, 64, 64), (24, 16, 128), (16, 24, 256),
+                                  (9, 12, 512)])
 def test_fd8_bit_exact_sizes(P, dims):
     """Ragged tiles, the minimum stencil size and magnitudes from 1e-38 to 1e30
     (the reciprocal division must reproduce IEEE division bit for bit)."""
@@ -79,6 +80,27 @@ def test_fd8_bit_exact_sizes(P, dims):
     np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), O.grad(f))
     w = (rng.standard_normal((3,) + dims)).astype(np.float32)
     np.testing.assert_array_equal(_np(P.fd8_divergence(P.VectorField(g, w)).values), O.div(w))
+
+
+@pytest.mark.parametrize("dims", [(32, 40, 128), (20, 32, 256), (12, 8, 512)])
+def test_fd8_row_kernel_matches_tile_kernel(P, dims):
+    """vr_set_fd8_mode A/B: the bulk-copy row-tile kernel and the cp.async tile
+    kernel give identical bits (gradient and divergence)."""
+    from paper_2209_08189_b200 import _lib
+    lib = _lib.lib()
+    g = P.make_grid(dims)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    f = torch.randn(dims, device="cuda", generator=gen) * 10.0
+    v = torch.randn((3,) + dims, device="cuda", generator=gen)
+    outs = {}
+    for mode in (0, 1):
+        prev = lib.vr_set_fd8_mode(mode)
+        try:
+            outs[mode] = (P.fd8_gradient(P.ScalarField(g, f)).data.clone(),
+                          P.fd8_divergence(P.VectorField(g, v)).values.clone())
+        finally:
+            lib.vr_set_fd8_mode(prev)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
 def test_fd8_requires_nine(P):

@@ -17,6 +17,25 @@ st = optim.ObjectiveState(m0, m1, P.VectorField(g, 0.5 * vtrue.data), cfg, ops)
 ms = st.m_series
 out = torch.empty((3,) + ms.shape[1:], device="cuda")
 rnd = torch.rand(ms.shape[1:], device="cuda")
+from paper_2209_08189_b200 import _lib
+lib = _lib.lib()
+flush = torch.empty(64 * 1024 * 1024, device="cuda")
+v3 = torch.randn((3,) + ms.shape[1:], device="cuda")
+dv = torch.empty(ms.shape[1:], device="cuda")
+for mode in (1, 0):
+    lib.vr_set_fd8_mode(mode)
+    for what, fn in (("grad", lambda: P.diffops.fd8_gradient_t(rnd, out=out)),
+                     ("div", lambda: P.diffops.fd8_divergence_t(v3, out=dv))):
+        ts = []
+        for _ in range(12):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); fn(); b.record(); b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = sorted(ts)[6]
+        print(f"mode {mode} {what}: {t:.4f} ms (L2 flushed), {16 * rnd.numel() / (t * 1e-3) / 1e9:.0f} GB/s algorithmic",
+              flush=True)
+lib.vr_set_fd8_mode(1)
 for name, f in [("rand", rnd)] + [(f"m{j}", ms[j]) for j in range(5)] + [("m4copy", ms[4].clone())]:
     for _ in range(2):
         P.diffops.fd8_gradient_t(f, out=out)
