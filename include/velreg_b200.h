@@ -97,10 +97,10 @@ int vr_set_spec_a_mode(int mode);
  * VR_ERR_ARG for an unknown key. */
 int vr_set_spectral_tuning(int key, int value);
 
-/* Tuning switch (no reference counterpart) for FD8: 1 (default) = row-tile
- * kernel staging whole x3 rows with cp.async.bulk (N3 in {128, 256, 512},
- * 16-byte-aligned fields), 0 = the cp.async tile kernel.  Bit-identical
- * results.  Returns the previous mode. */
+/* Tuning switch (no reference counterpart) for FD8: 0 (default) = the
+ * cp.async tile kernel, 1 = row-tile kernel staging whole x3 rows with
+ * cp.async.bulk (N3 in {128, 256}, 16-byte-aligned fields; measured slower).
+ * Bit-identical results.  Returns the previous mode. */
 int vr_set_fd8_mode(int mode);
 
 /* Number of kernel launches one vr_spec_apply(p, kind, ., ncomp, ...) makes

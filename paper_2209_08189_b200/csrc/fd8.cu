@@ -53,29 +53,17 @@ __device__ __forceinline__ float fd8_sum(float p0, float p1, float p2, float p3,
   return out;
 }
 
-// The 12 sums of one micro-tile step (x1 / x2 / x3 derivative, 4 voxels each)
-// divided by h: IEEE division where the reciprocal form is not proven exact.
-struct F12 {
-  float v[12];
-};
-__device__ __noinline__ F12 fd8_div_ieee(F12 s, float h1, float h2, float h3, float r1, float r2, float r3,
-                                         unsigned dlo, unsigned dspan) {
-  // Tiny sums with a normal quotient (2^-125 <= |x/h|, |x| < 2^-100) are
-  // scaled by 2^64 into the verified range first: both scalings are exact.
-  const bool verified = dlo == 0x0d800000u;
-  F12 o;
-#pragma unroll
-  for (int i = 0; i < 12; ++i) {
-    const float h = i < 4 ? h1 : (i < 8 ? h2 : h3), r = i < 4 ? r1 : (i < 8 ? r2 : r3);
-    const float x = s.v[i], ax = fabsf(x);
-    if (!div_needs_ieee(x, dlo, dspan))
-      o.v[i] = div_fast(x, h, r);
-    else if (verified && ax < 0x1p-100f && ax >= 0x1p-125f * h)
-      o.v[i] = __fmul_rn(div_fast(__fmul_rn(x, 0x1p64f), h, r), 0x1p-64f);
-    else
-      o.v[i] = __fdiv_rn(x, h);
-  }
-  return o;
+// One quotient outside the reciprocal form's proven range.  Tiny sums with a
+// normal quotient (2^-125 <= |x/h|, |x| < 2^-100) are scaled by 2^64 into the
+// verified range first (both scalings are exact); the rest take IEEE division.
+__device__ __noinline__ float fd8_div_slow(float x, float h, float r, unsigned dlo) {
+  const float ax = fabsf(x);
+  if (dlo == 0x0d800000u && ax < 0x1p-100f && ax >= 0x1p-125f * h)
+    return __fmul_rn(div_fast(__fmul_rn(x, 0x1p64f), h, r), 0x1p-64f);
+  return __fdiv_rn(x, h);
+}
+__device__ __forceinline__ float fd8_div(float x, float h, float r, unsigned dlo, unsigned dspan) {
+  return div_needs_ieee(x, dlo, dspan) ? fd8_div_slow(x, h, r, dlo) : div_fast(x, h, r);
 }
 
 template <int V>
@@ -305,43 +293,16 @@ __global__ void __launch_bounds__(NTHR, 2) fd8_kernel(const float* __restrict__ 
           }
         }
       }
-      // out /= h (diffops.py:96): reciprocal division unless an operand is extreme
-      bool ieee = false;
+      // out /= h (diffops.py:96): reciprocal division; IEEE (out of line, per
+      // element) only for the rare quotients outside the proven range
 #pragma unroll
       for (int r = 0; r < RY; ++r)
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
-                  div_needs_ieee(g3[r][c], dlo, dspan);
-      if (ieee) {  // rare: out of line, so the 9 unrolled steps stay compact
-        F12 sv;
-#pragma unroll
-        for (int r = 0; r < RY; ++r)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            sv.v[r * 2 + c] = g1[r][c];
-            sv.v[4 + r * 2 + c] = g2[r][c];
-            sv.v[8 + r * 2 + c] = g3[r][c];
-          }
-        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
-#pragma unroll
-        for (int r = 0; r < RY; ++r)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            g1[r][c] = sv.v[r * 2 + c];
-            g2[r][c] = sv.v[4 + r * 2 + c];
-            g3[r][c] = sv.v[8 + r * 2 + c];
-          }
-      } else {
-#pragma unroll
-        for (int r = 0; r < RY; ++r)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            g1[r][c] = div_fast(g1[r][c], h1, r1);
-            g2[r][c] = div_fast(g2[r][c], h2, r2);
-            g3[r][c] = div_fast(g3[r][c], h3, r3);
-          }
-      }
+        for (int c = 0; c < 2; ++c) {
+          g1[r][c] = fd8_div(g1[r][c], h1, r1, dlo, dspan);
+          g2[r][c] = fd8_div(g2[r][c], h2, r2, dlo, dspan);
+          g3[r][c] = fd8_div(g3[r][c], h3, r3, dlo, dspan);
+        }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         if (!act[r]) continue;
@@ -558,41 +519,16 @@ __global__ void __launch_bounds__(256, 2) fd8_rows_kernel(const float* __restric
       }
     }
     __syncthreads();   // every reader of stage s is done: the next issue() may refill it
-    bool ieee = false;
+    // out /= h: reciprocal division, IEEE (out of line, per element) only for
+    // the rare quotients outside the proven range
 #pragma unroll
     for (int r = 0; r < RY; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
-                div_needs_ieee(g3[r][c], dlo, dspan);
-    if (ieee) {
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        F12 sv;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          sv.v[c] = g1[r][c];
-          sv.v[4 + c] = g2[r][c];
-          sv.v[8 + c] = g3[r][c];
-        }
-        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          g1[r][c] = sv.v[c];
-          g2[r][c] = sv.v[4 + c];
-          g3[r][c] = sv.v[8 + c];
-        }
+      for (int c = 0; c < 4; ++c) {
+        g1[r][c] = fd8_div(g1[r][c], h1, r1, dlo, dspan);
+        g2[r][c] = fd8_div(g2[r][c], h2, r2, dlo, dspan);
+        g3[r][c] = fd8_div(g3[r][c], h3, r3, dlo, dspan);
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < RY; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          g1[r][c] = div_fast(g1[r][c], h1, r1);
-          g2[r][c] = div_fast(g2[r][c], h2, r2);
-          g3[r][c] = div_fast(g3[r][c], h3, r3);
-        }
-    }
     float* op = out + (int64_t)i * psz;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
@@ -643,8 +579,12 @@ void fd8_rows_run(cudaStream_t s, const float* in, const float* lo, const float*
                                                                     dspan, out, nchunk);
 }
 
-// 0: cp.async tile kernel only; 1 (default): row-tile bulk-copy kernel where it applies
-static int g_fd8_mode = 1;
+// 0 (default): cp.async tile kernel; 1: row-tile bulk-copy kernel where it applies
+// (N3 in {128, 256}).  Measured on B200 at 256^3 with the L2 flushed: row
+// kernel gradient 0.092 ms / divergence 0.145 ms vs tile kernel 0.084 / 0.085 ms
+// (one barrier + mbarrier wait per plane for all 8 warps, and the 8-plane
+// window preload per 16-plane chunk), so the tile kernel stays the default.
+static int g_fd8_mode = 0;
 
 template <int MODE, bool SLAB>
 bool fd8_rows_dispatch(cudaStream_t s, const float* in, const float* lo, const float* hi, Dims d, float h1,
@@ -656,8 +596,6 @@ bool fd8_rows_dispatch(cudaStream_t s, const float* in, const float* lo, const f
       fd8_rows_run<MODE, SLAB, 128>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
     case 256: if (d.n2 % RowCfg<256>::TY) return false;
       fd8_rows_run<MODE, SLAB, 256>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
-    case 512: if (d.n2 % RowCfg<512>::TY) return false;
-      fd8_rows_run<MODE, SLAB, 512>(s, in, lo, hi, d, h1, h2, h3, r1, r2, r3, dlo, dspan, out); return true;
     default: return false;
   }
 }

@@ -82,7 +82,7 @@ def test_fd8_bit_exact_sizes(P, dims):
     np.testing.assert_array_equal(_np(P.fd8_divergence(P.VectorField(g, w)).values), O.div(w))
 
 
-@pytest.mark.parametrize("dims", [(32, 40, 128), (20, 32, 256), (12, 8, 512)])
+@pytest.mark.parametrize("dims", [(32, 40, 128), (20, 32, 256)])
 def test_fd8_row_kernel_matches_tile_kernel(P, dims):
     """vr_set_fd8_mode A/B: the bulk-copy row-tile kernel and the cp.async tile
     kernel give identical bits (gradient and divergence)."""
