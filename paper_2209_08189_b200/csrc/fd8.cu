@@ -53,17 +53,29 @@ __device__ __forceinline__ float fd8_sum(float p0, float p1, float p2, float p3,
   return out;
 }
 
-// One quotient outside the reciprocal form's proven range.  Tiny sums with a
-// normal quotient (2^-125 <= |x/h|, |x| < 2^-100) are scaled by 2^64 into the
-// verified range first (both scalings are exact); the rest take IEEE division.
-__device__ __noinline__ float fd8_div_slow(float x, float h, float r, unsigned dlo) {
-  const float ax = fabsf(x);
-  if (dlo == 0x0d800000u && ax < 0x1p-100f && ax >= 0x1p-125f * h)
-    return __fmul_rn(div_fast(__fmul_rn(x, 0x1p64f), h, r), 0x1p-64f);
-  return __fdiv_rn(x, h);
-}
-__device__ __forceinline__ float fd8_div(float x, float h, float r, unsigned dlo, unsigned dspan) {
-  return div_needs_ieee(x, dlo, dspan) ? fd8_div_slow(x, h, r, dlo) : div_fast(x, h, r);
+// The 12 sums of one micro-tile step (x1 / x2 / x3 derivative, 4 voxels each)
+// divided by h: IEEE division where the reciprocal form is not proven exact.
+struct F12 {
+  float v[12];
+};
+__device__ __noinline__ F12 fd8_div_ieee(F12 s, float h1, float h2, float h3, float r1, float r2, float r3,
+                                         unsigned dlo, unsigned dspan) {
+  // Tiny sums with a normal quotient (2^-125 <= |x/h|, |x| < 2^-100) are
+  // scaled by 2^64 into the verified range first: both scalings are exact.
+  const bool verified = dlo == 0x0d800000u;
+  F12 o;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const float h = i < 4 ? h1 : (i < 8 ? h2 : h3), r = i < 4 ? r1 : (i < 8 ? r2 : r3);
+    const float x = s.v[i], ax = fabsf(x);
+    if (!div_needs_ieee(x, dlo, dspan))
+      o.v[i] = div_fast(x, h, r);
+    else if (verified && ax < 0x1p-100f && ax >= 0x1p-125f * h)
+      o.v[i] = __fmul_rn(div_fast(__fmul_rn(x, 0x1p64f), h, r), 0x1p-64f);
+    else
+      o.v[i] = __fdiv_rn(x, h);
+  }
+  return o;
 }
 
 template <int V>
@@ -293,16 +305,43 @@ __global__ void __launch_bounds__(NTHR, 2) fd8_kernel(const float* __restrict__ 
           }
         }
       }
-      // out /= h (diffops.py:96): reciprocal division; IEEE (out of line, per
-      // element) only for the rare quotients outside the proven range
+      // out /= h (diffops.py:96): reciprocal division unless an operand is extreme
+      bool ieee = false;
 #pragma unroll
       for (int r = 0; r < RY; ++r)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          g1[r][c] = fd8_div(g1[r][c], h1, r1, dlo, dspan);
-          g2[r][c] = fd8_div(g2[r][c], h2, r2, dlo, dspan);
-          g3[r][c] = fd8_div(g3[r][c], h3, r3, dlo, dspan);
-        }
+        for (int c = 0; c < 2; ++c)
+          ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
+                  div_needs_ieee(g3[r][c], dlo, dspan);
+      if (ieee) {  // rare: out of line, so the 9 unrolled steps stay compact
+        F12 sv;
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            sv.v[r * 2 + c] = g1[r][c];
+            sv.v[4 + r * 2 + c] = g2[r][c];
+            sv.v[8 + r * 2 + c] = g3[r][c];
+          }
+        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            g1[r][c] = sv.v[r * 2 + c];
+            g2[r][c] = sv.v[4 + r * 2 + c];
+            g3[r][c] = sv.v[8 + r * 2 + c];
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            g1[r][c] = div_fast(g1[r][c], h1, r1);
+            g2[r][c] = div_fast(g2[r][c], h2, r2);
+            g3[r][c] = div_fast(g3[r][c], h3, r3);
+          }
+      }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         if (!act[r]) continue;
@@ -519,16 +558,41 @@ __global__ void __launch_bounds__(256, 2) fd8_rows_kernel(const float* __restric
       }
     }
     __syncthreads();   // every reader of stage s is done: the next issue() may refill it
-    // out /= h: reciprocal division, IEEE (out of line, per element) only for
-    // the rare quotients outside the proven range
+    bool ieee = false;
 #pragma unroll
     for (int r = 0; r < RY; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        g1[r][c] = fd8_div(g1[r][c], h1, r1, dlo, dspan);
-        g2[r][c] = fd8_div(g2[r][c], h2, r2, dlo, dspan);
-        g3[r][c] = fd8_div(g3[r][c], h3, r3, dlo, dspan);
+      for (int c = 0; c < 4; ++c)
+        ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
+                div_needs_ieee(g3[r][c], dlo, dspan);
+    if (ieee) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        F12 sv;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          sv.v[c] = g1[r][c];
+          sv.v[4 + c] = g2[r][c];
+          sv.v[8 + c] = g3[r][c];
+        }
+        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g1[r][c] = sv.v[c];
+          g2[r][c] = sv.v[4 + c];
+          g3[r][c] = sv.v[8 + c];
+        }
       }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g1[r][c] = div_fast(g1[r][c], h1, r1);
+          g2[r][c] = div_fast(g2[r][c], h2, r2);
+          g3[r][c] = div_fast(g3[r][c], h3, r3);
+        }
+    }
     float* op = out + (int64_t)i * psz;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
@@ -584,6 +648,8 @@ void fd8_rows_run(cudaStream_t s, const float* in, const float* lo, const float*
 // kernel gradient 0.092 ms / divergence 0.145 ms vs tile kernel 0.084 / 0.085 ms
 // (one barrier + mbarrier wait per plane for all 8 warps, and the 8-plane
 // window preload per 16-plane chunk), so the tile kernel stays the default.
+// (A per-element inline IEEE-division select was also measured: 0.094 ms --
+// the one-branch-per-micro-tile form below is faster on the common path.)
 static int g_fd8_mode = 0;
 
 template <int MODE, bool SLAB>
