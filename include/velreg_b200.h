@@ -187,6 +187,17 @@ int vr_axpby(int64_t n, double a, const float* x, double b, const float* y, floa
 int vr_pcg_update(int64_t n, double alpha, const float* p, const float* hp, float* x, float* r, void* stream);
 int vr_fill(int64_t n, float value, float* out, void* stream);
 
+/* ---- SYN benchmark template (synth.py:77-101 make_template) -------------------
+ * labels / image (either may be NULL) of x1 planes [x_begin, x_begin + x_count)
+ * of the global lattice dims: the largest shape index s + 1 whose star shape
+ * |u| <= norm |P_l^m(cos(phi(u) + phi_hat_s))| covers the voxel, u = (x - pi)
+ * - c_s; or |u| <= fixed_radius when fixed_radius >= 0.  shapes_host: HOST
+ * doubles {c1, c2, c3, phi_hat} per shape (the reference's default_rng draws);
+ * norm = |Y_l^m| normalisation, dfact_m = (2m-1)!! (host f64, synth.py:51,69). */
+int vr_syn_template(const int64_t dims[3], int x_begin, int x_count, const double* shapes_host, int nshapes, int l,
+                    int m, double norm, double dfact_m, double fixed_radius, int* labels, float* image,
+                    void* stream);
+
 /* (min l0, max l0, min l1, max l1) of one or two int32 label maps (l1 may be
  * NULL), written to out[4] (int32, device).  Validates label ids (grid.py
  * LabelMap, non-negative) and sizes vr_label_counts with one host read. */

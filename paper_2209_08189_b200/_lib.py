@@ -65,6 +65,7 @@ _SIGS = {
     "vr_fill": [_i64, _f32, _p, _p],
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
     "vr_label_range": [_p, _p, _i64, _p, _p],
+    "vr_syn_template": [_dims_t, _i32, _i32, _p, _i32, _i32, _i32, _f64, _f64, _f64, _p, _p, _p],
     # x1-slab / distributed
     "vr_trace_rk2_slab": [_p, _dims_t, _i64, _i32, _f64, _i32, _p, _p, _p, _p, _p, _p],
     "vr_advect_slab": [_p, _p, _p, _dims_t, _i32, _p, _p, _i32, _p, _p, _i32, _i32, _p],

@@ -10,6 +10,7 @@ SURVEY.md §8(d) (the blob pair and the sphere -> deformed sphere pair).
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -17,6 +18,113 @@ import torch
 from . import _lib
 from .grid import Grid, LabelMap, ScalarField, VectorField
 from .transport import TransportConfig, TransportOperators, solve_state
+
+
+# ---- SYN benchmark (synth.py:22-101; §4 "SYN") ------------------------
+@dataclass
+class SynthSpec:
+    """synth.py:22-39: shape count, spherical-harmonic degree / order,
+    velocity frequency K, seed, and the constant-radius test hook."""
+    grid: Grid
+    num_shapes: int = 10
+    degree: int = 8
+    order: int = 6
+    velocity_frequency: int = 4
+    seed: int = 0
+    fixed_radius: float = None
+
+    def __post_init__(self):
+        if self.num_shapes < 1:
+            raise ValueError("num_shapes must be >= 1")
+        if not 0 <= self.order <= self.degree:
+            raise ValueError("need 0 <= order <= degree")
+        if self.velocity_frequency < 1:
+            raise ValueError("velocity frequency K must be >= 1")
+
+
+def assoc_legendre(l: int, m: int, x) -> np.ndarray:
+    """Associated Legendre P_l^m with Condon-Shortley phase, upward recurrence
+    (synth.py:42-62); host numpy utility -- the device template evaluates the
+    same recurrence per voxel (csrc/synth.cu)."""
+    if not 0 <= m <= l:
+        raise ValueError(f"need 0 <= m <= l, got l={l}, m={m}")
+    x = np.asarray(x, dtype=np.float64)
+    if np.any(np.abs(x) > 1.0 + 1e-14):
+        raise ValueError("associated Legendre argument must satisfy |x| <= 1")
+    pmm = np.ones_like(x)
+    if m > 0:
+        s = np.sqrt(np.clip(1.0 - x * x, 0.0, None))
+        pmm = (-1.0) ** m * float(math.prod(range(1, 2 * m, 2))) * s ** m
+    if l == m:
+        return pmm
+    pm1 = x * (2 * m + 1) * pmm
+    if l == m + 1:
+        return pm1
+    for ll in range(m + 2, l + 1):
+        pmm, pm1 = pm1, (x * (2 * ll - 1) * pm1 - (ll + m - 1) * pmm) / (ll - m)
+    return pm1
+
+
+def _sh_norm(l: int, m: int) -> float:
+    return math.sqrt((2 * l + 1) / (4.0 * math.pi) * math.factorial(l - m) / math.factorial(l + m))
+
+
+def spherical_harmonic_magnitude(l: int, m: int, theta, phi) -> np.ndarray:
+    """|Y_l^m(theta, phi)| (synth.py:65-74): the azimuth only enters a
+    unit-modulus phase."""
+    del theta
+    return _sh_norm(l, m) * np.abs(assoc_legendre(l, m, np.cos(phi)))
+
+
+QUARTER_TURNS = (0.0, 0.5 * math.pi, math.pi, 1.5 * math.pi)
+OFFSET_BOUND = 0.4 * math.pi
+
+
+def _syn_shapes(spec: SynthSpec) -> np.ndarray:
+    """The reference's random draws, in its order (synth.py:88-92): per shape
+    a centre in [-0.4 pi, 0.4 pi]^3 and two quarter turns (the azimuthal one
+    is drawn but cancels in |Y_l^m|).  Rows {c1, c2, c3, phi_hat}."""
+    rng = np.random.default_rng(spec.seed)
+    rows = []
+    for _ in range(spec.num_shapes):
+        center = rng.uniform(-OFFSET_BOUND, OFFSET_BOUND, size=3)
+        _theta_hat = QUARTER_TURNS[rng.integers(0, 4)]
+        phi_hat = QUARTER_TURNS[rng.integers(0, 4)]
+        rows.append([center[0], center[1], center[2], phi_hat])
+    return np.ascontiguousarray(rows, dtype=np.float64)
+
+
+def make_template(spec: SynthSpec):
+    """Template image (the label ids as intensities) and its label map
+    (synth.py:77-101), evaluated on the device -- one thread per voxel over all
+    shapes (csrc/synth.cu) -- for this rank's x1 slab when a decomposition of
+    the grid is active."""
+    from . import dist
+    grid = spec.grid
+    ctx = dist.for_grid(grid.dims)
+    x0, nx = (ctx.x0, ctx.L1) if ctx is not None else (0, grid.dims[0])
+    shape = (nx,) + tuple(grid.dims[1:])
+    labels = torch.empty(shape, dtype=torch.int32, device=_lib.device())
+    image = torch.empty(shape, dtype=torch.float32, device=labels.device)
+    shapes = _syn_shapes(spec)
+    fixed = -1.0 if spec.fixed_radius is None else float(spec.fixed_radius)
+    l, m = spec.degree, spec.order
+    rc = _lib.lib().vr_syn_template(_lib.dims_arg(grid.dims), int(x0), int(nx), shapes.ctypes.data,
+                                    int(shapes.shape[0]), int(l), int(m), _sh_norm(l, m),
+                                    float(math.prod(range(1, 2 * m, 2))), fixed, labels.data_ptr(),
+                                    image.data_ptr(), _lib.stream())
+    _lib.check(rc, "vr_syn_template")
+    return ScalarField(grid, image), LabelMap(grid, labels, spec.num_shapes)
+
+
+def make_syn_problem(spec: SynthSpec, n_t: int = 4, order: str = "cubic"):
+    """SYN pair (SPEC.md synthgen, §4): template + labels, velocity
+    make_velocity(K) evaluated on the device, reference image and labels by
+    transport (synth.py:134-141).  Returns (m0, m1, labels0, labels1, v)."""
+    m0, l0 = make_template(spec)
+    v = VectorField(spec.grid, velocity_tensor(spec.velocity_frequency, spec.grid))
+    m1, l1 = make_reference(m0, l0, v, TransportConfig(n_t, order))
+    return m0, m1, l0, l1, v
 
 
 def make_velocity(K: int, grid: Grid) -> VectorField:
@@ -141,9 +249,14 @@ def c2_problem(grid: Grid, order: str = "cubic", n_t: int = 4):
 
 
 def _device_axes(grid: Grid):
-    """Broadcastable f64 lattice coordinates on the device: (N1,1,1), (1,N2,1), (1,1,N3)."""
+    """Broadcastable f64 lattice coordinates on the device: (L1,1,1), (1,N2,1),
+    (1,1,N3) -- this rank's x1 planes when a decomposition of the grid is active."""
+    from . import dist
     dev = _lib.device()
     ax = [torch.arange(n, dtype=torch.float64, device=dev) * (2 * math.pi / n) for n in grid.dims]
+    ctx = dist.for_grid(grid.dims)
+    if ctx is not None:
+        ax[0] = ax[0][ctx.x0:ctx.x0 + ctx.L1]
     return ax[0].view(-1, 1, 1), ax[1].view(1, -1, 1), ax[2].view(1, 1, -1)
 
 
@@ -155,9 +268,10 @@ def velocity_tensor(K: int, grid: Grid, scale: float = 1.0) -> torch.Tensor:
         raise ValueError("K must be >= 1")
     x, y, z = _device_axes(grid)
     xc, yc, zc = x - math.pi, y - math.pi, z - math.pi
-    out = torch.empty((3,) + tuple(grid.dims), dtype=torch.float32, device=x.device)
+    shape = (x.shape[0],) + tuple(grid.dims[1:])
+    out = torch.empty((3,) + shape, dtype=torch.float32, device=x.device)
     for c in range(3):
-        acc = torch.zeros(grid.dims, dtype=torch.float64, device=x.device)
+        acc = torch.zeros(shape, dtype=torch.float64, device=x.device)
         for k in range(1, K + 1):
             a = k ** -0.5
             if c == 0:
