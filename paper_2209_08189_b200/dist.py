@@ -103,6 +103,10 @@ class SlabContext:
             tdist.all_reduce(t, op=rop, group=self.group)
         return t
 
+    def barrier(self) -> None:
+        if self.world > 1:
+            tdist.barrier(group=self.group)
+
     # ---- ghost planes --------------------------------------------------------------
     def ghosts(self, x: torch.Tensor, w: int) -> tuple:
         """(lo, hi) ghost blocks (..., w, N2, N3) of the local slab x (..., L1, N2, N3):
