@@ -5,7 +5,7 @@ import paper_2209_08189_b200 as P
 
 
 def test_public_names_match_reference_surface():
-    # the solver-path names re-exported by velreg/__init__.py:10-33
+    # every name velreg/__init__.py:10-33 re-exports
     for name in ["GridError", "ObjectiveError", "ResampleError", "SearchError", "TransportError", "VelregError",
                  "VolumeIOError", "Grid", "LabelMap", "ScalarField", "VectorField", "make_grid",
                  "prolong_spectral", "restrict", "RegOperators", "SpectralWorkspace", "apply_A", "apply_K",
@@ -17,7 +17,8 @@ def test_public_names_match_reference_surface():
                  "reduced_gradient", "relative_residual", "make_reference", "make_velocity", "transport_labels",
                  "DiceReport", "dice", "dice_averages", "jacobian_stats", "residual_image", "register", "SearchConfig", "SearchResult",
                  "continuation_register", "in_bounds", "search_beta_v", "search_beta_w", "search_parameters",
-                 "ExperimentPlan", "run_experiment"]:
+                 "ExperimentPlan", "run_experiment", "SynthSpec", "assoc_legendre", "make_template",
+                 "spherical_harmonic_magnitude", "load_nifti", "load_volume", "save_volume"]:
         assert hasattr(P, name), name
 
 
