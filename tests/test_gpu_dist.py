@@ -123,6 +123,74 @@ def case_c2_64(rank, world):
     assert abs(res.dice.d_a - gold["dice_post"]) < 0.005
 
 
+def _dist_vs_single(rank, world, n, order):
+    """Every operator and a full C2 registration on x1 slabs against the
+    single-domain result on the same GPU (identical float32 inputs, made on
+    the device): global relative L2 <= 1e-6 per operator (allreduced), PCG
+    counts identical, objective / residual / J extrema / Dice within 1e-6."""
+    import torch.distributed as tdist
+    import paper_2209_08189_b200 as P
+    from paper_2209_08189_b200 import dist
+    from paper_2209_08189_b200.synth import c2_problem_device
+    g = P.make_grid((n, n, n))
+    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=1e-4, n_t=4, interp_order=order)
+    m0, m1, l0, l1, vtrue = c2_problem_device(g, order, 4)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    w = 0.1 * torch.randn((3,) + g.dims, device="cuda", generator=gen)
+    v = P.VectorField(g, 0.5 * vtrue.data)
+
+    def ops_list(vv, ww, mm0, mm1, ctx):
+        ops = P.RegOperators.for_grid(g, cfg.beta_v, cfg.beta_w)
+        W = P.VectorField(g, ww)
+        st = P.ObjectiveState(mm0, mm1, vv, cfg, ops)
+        return {"A": P.apply_A(W, ops).data, "K": P.apply_K(W, ops).data,
+                "invshift": P.apply_inv_shifted_A(W, ops, 1.0).data,
+                "grad_m0": P.fd8_gradient(mm0).data, "div_v": P.fd8_divergence(vv).values,
+                "disp_fwd": st.transport_ops.forward.displacement, "disp_bwd": st.transport_ops.backward.displacement,
+                "state": st.m_series[-1], "adjoint": st.lambda_series[0], "gradient": st.gradient.data,
+                "matvec": P.hessian_matvec(W, st).data, "objective": torch.tensor([st.objective], device="cuda")}
+
+    single = ops_list(v, w, m0, m1, None)
+    ref = P.register(m0, m1, cfg, labels0=l0, labels1=l1)
+    ctx = dist.SlabContext(g.dims)
+    sl = slice(ctx.x0, ctx.x0 + ctx.L1)
+    with dist.activate(ctx):
+        def loc(x):
+            return x[..., sl, :, :].contiguous()
+        V = P.VectorField(g, loc(v.data))
+        M0, M1 = P.ScalarField(g, loc(m0.values)), P.ScalarField(g, loc(m1.values))
+        slab = ops_list(V, loc(w), M0, M1, ctx)
+        res = P.register(M0, M1, cfg, labels0=P.LabelMap(g, loc(l0.labels)), labels1=P.LabelMap(g, loc(l1.labels)))
+    errs = {}
+    for k, a in slab.items():
+        b = single[k] if k == "objective" else single[k][..., sl, :, :]
+        nd = torch.tensor([float(torch.sum((a.double() - b.double()) ** 2)), float(torch.sum(b.double() ** 2))],
+                          dtype=torch.float64, device="cuda")
+        if k != "objective":
+            tdist.all_reduce(nd)
+        errs[k] = float((nd[0] / nd[1]).sqrt())
+    bad = {k: e for k, e in errs.items() if not e <= 1e-6}
+    assert not bad, (rank, errs)
+    d0, d1 = ref.diagnostics, res.diagnostics
+    assert [r.pcg_iterations for r in d0.iterations] == [r.pcg_iterations for r in d1.iterations]
+    assert d0.termination_reason == d1.termination_reason
+    for a, b in ((d0.relative_residual, d1.relative_residual), (d0.j_min, d1.j_min), (d0.j_max, d1.j_max),
+                 (d0.iterations[-1].objective, d1.iterations[-1].objective), (ref.dice.d_a, res.dice.d_a)):
+        assert abs(a / b - 1) < 1e-6, (a, b)
+    if rank == 0:
+        print(f"dist-vs-single n={n} {order} world={world}: max operator rel L2 {max(errs.values()):.2e} "
+              f"({max(errs, key=errs.get)}); PCG {[r.pcg_iterations for r in d1.iterations]}; residual "
+              f"{d1.relative_residual:.9e} vs {d0.relative_residual:.9e}; Dice {res.dice.d_a:.9f}", flush=True)
+
+
+def case_parity_256(rank, world):
+    _dist_vs_single(rank, world, 256, "cubic")
+
+
+def case_parity_512(rank, world):
+    _dist_vs_single(rank, world, 512, "linear")
+
+
 @pytest.mark.parametrize("case", ["case_ops_match_single", "case_gn32", "case_c2_64"])
 def test_slab_world1(case):
     spawn(case, 1)
@@ -132,3 +200,15 @@ def test_slab_world1(case):
 @pytest.mark.parametrize("case", ["case_gn32", "case_c2_64"])
 def test_slab_world2(case):
     spawn(case, 2)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (gpurun --gpus 2)")
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512"])
+def test_dist_vs_single_world2(case):
+    spawn(case, 2)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs (gpurun --gpus 4)")
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512"])
+def test_dist_vs_single_world4(case):
+    spawn(case, 4)
