@@ -254,6 +254,23 @@ int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_globa
 int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
                      void* stream);
 
+/* ---- peer-memory transport (multi-GPU, one process per GPU; dist.py) ---------
+ * Symmetric buffers: vr_peer_malloc allocates (zeroed) device memory and
+ * returns its CUDA IPC handle (vr_peer_handle_bytes() bytes, host memory);
+ * peers map it with vr_peer_open.  vr_peer_copy = copy-engine D2D copy (dst
+ * may be a peer mapping).  vr_peer_signal stores `value` into a (peer) uint64
+ * flag after all prior work on `stream` (system-scope release);
+ * vr_peer_wait makes `stream` wait until a local flag >= value
+ * (cuStreamWaitValue64; VR_ERR_UNSUPPORTED without stream memory ops). */
+int vr_peer_malloc(int64_t bytes, void** ptr, void* handle_out);
+int vr_peer_free(void* ptr);
+int vr_peer_open(const void* handle, void** ptr);
+int vr_peer_close(void* ptr);
+int vr_peer_handle_bytes(void);
+int vr_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
+int vr_peer_signal(unsigned long long* flag, unsigned long long value, void* stream);
+int vr_peer_wait(const unsigned long long* flag, unsigned long long value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

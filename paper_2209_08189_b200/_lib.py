@@ -78,6 +78,15 @@ _SIGS = {
     "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _i32, _p, _p, _p],
     "vr_dspec_h1_partial": [_p, _p, _i32, _i32, _i32, _f64, _p, _p],
     "vr_dspec_inverse": [_p, _p, _i32, _i32, _p, _p, _p],
+    # peer-memory transport
+    "vr_peer_malloc": [_i64, C.POINTER(_p), _p],
+    "vr_peer_free": [_p],
+    "vr_peer_open": [_p, C.POINTER(_p)],
+    "vr_peer_close": [_p],
+    "vr_peer_handle_bytes": [],
+    "vr_peer_copy": [_p, _p, _i64, _p],
+    "vr_peer_signal": [_p, C.c_uint64, _p],
+    "vr_peer_wait": [_p, C.c_uint64, _p],
 }
 
 EXPORTED = tuple(_SIGS)
@@ -98,7 +107,9 @@ LAUNCHES = {"vr_spec_apply_launches": 0, "vr_h1_energy": 4, "vr_prolong_spectral
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
             "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
-            "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0}
+            "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0,
+            "vr_peer_malloc": 0, "vr_peer_free": 0, "vr_peer_open": 0, "vr_peer_close": 0, "vr_peer_handle_bytes": 0,
+            "vr_peer_copy": 0, "vr_peer_wait": 0}
 
 
 class Profile:

@@ -1,0 +1,117 @@
+// Peer-memory transport between the GPUs of one node (one process per GPU).
+//
+// The x1-slab decomposition (dist.py) moves data between ranks at three kinds
+// of points: ghost planes for the stencils, the spectral transposes, and
+// scalar reductions.  The first two run here over NVLink / NVSwitch without
+// NCCL kernels:
+//   * symmetric buffers: cudaMalloc'd receive buffers whose CUDA IPC handles
+//     every rank opens, so a rank can store straight into a peer's buffer;
+//   * ghost planes: copy-engine copies (cudaMemcpyAsync on a side stream --
+//     no SMs taken from the sweep kernels that overlap them);
+//   * transposes: the spectral pack / x1 kernels store their output tiles
+//     directly into the destination rank's receive buffer (spectral.cu,
+//     vr_dspec_*_peer) -- the transpose IS the kernel's epilogue;
+//   * completion: per (source, channel) uint64 epoch flags in the receiver's
+//     memory, written by the sender after its data (a one-thread release-store
+//     kernel ordered behind the copy / producer kernel, system-scope fence
+//     first) and awaited on the receiver's stream with cuStreamWaitValue64
+//     (no spinning kernel, no host round trip).
+// Epochs only grow, so flags are never reset; a receive buffer is reused only
+// after a later exchange with the same peer has completed.
+#include <cuda.h>
+#include <cstring>
+#include <mutex>
+#include "common.cuh"
+#include "../../include/velreg_b200.h"
+
+namespace {
+
+typedef CUresult (*PFN_waitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+PFN_waitValue64 g_wait = nullptr;
+std::once_flag g_once;
+
+void load_driver_entry_points() {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_wait = reinterpret_cast<PFN_waitValue64>(fn);
+  });
+}
+
+// one-thread release store of an epoch into a (peer) flag, after a
+// system-scope fence: everything this stream wrote before is visible first
+__global__ void signal_kernel(unsigned long long* flag, unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+}  // namespace
+
+extern "C" {
+
+int vr_peer_malloc(int64_t bytes, void** ptr, void* handle_out) {
+  if (bytes <= 0 || !ptr || !handle_out) return VR_ERR_ARG;
+  void* p = nullptr;
+  if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) return VR_ERR_ALLOC;
+  if (cudaMemset(p, 0, (size_t)bytes) != cudaSuccess ||
+      cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out), p) != cudaSuccess) {
+    cudaFree(p);
+    return VR_ERR_ALLOC;
+  }
+  *ptr = p;
+  return VR_OK;
+}
+
+int vr_peer_free(void* ptr) {
+  if (ptr) cudaFree(ptr);
+  return VR_OK;
+}
+
+int vr_peer_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return VR_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return VR_ERR_ALLOC;
+  *ptr = p;
+  return VR_OK;
+}
+
+int vr_peer_close(void* ptr) {
+  if (ptr) cudaIpcCloseMemHandle(ptr);
+  return VR_OK;
+}
+
+int vr_peer_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+// device-to-device copy on the copy engines (the destination may be a peer's
+// IPC-mapped buffer)
+int vr_peer_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes && (!dst || !src))) return VR_ERR_ARG;
+  if (!bytes) return VR_OK;
+  if (cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+    return VR_ERR_LAUNCH;
+  return VR_OK;
+}
+
+// flag := value, ordered after all prior work of `stream` (flag may be a peer's)
+int vr_peer_signal(unsigned long long* flag, unsigned long long value, void* stream) {
+  if (!flag) return VR_ERR_ARG;
+  signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// `stream` waits until *flag >= value (flag in this GPU's memory)
+int vr_peer_wait(const unsigned long long* flag, unsigned long long value, void* stream) {
+  if (!flag) return VR_ERR_ARG;
+  load_driver_entry_points();
+  if (!g_wait) return VR_ERR_UNSUPPORTED;
+  const CUresult r = g_wait((CUstream)stream, (CUdeviceptr)flag, (cuuint64_t)value, CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? VR_OK : VR_ERR_LAUNCH;
+}
+
+}  // extern "C"

@@ -110,9 +110,9 @@ class DistSpectralWorkspace:
         nc = 3 * ctx.L1 * n2 * self.n3h          # complex elements per 3-component slab spectrum
         dev = _lib.device()
         self.send = torch.empty(2 * nc, dtype=torch.float64, device=dev)
-        self.recv = torch.empty(2 * nc, dtype=torch.float64, device=dev)
+        self.recv = ctx.buffer(f"spec_recv_{n1}x{n2}x{n3}", torch.float64, 2 * nc)     # peers write here
         self.xout = torch.empty(2 * nc, dtype=torch.float32, device=dev)
-        self.irecv = torch.empty(2 * nc, dtype=torch.float32, device=dev)
+        self.irecv = ctx.buffer(f"spec_irecv_{n1}x{n2}x{n3}", torch.float32, 2 * nc)
         self.per_comp = ctx.L1 * n2 * self.n3h   # complex elements per component
         self.device = torch.cuda.current_device()
 

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import contextlib
 import math
+import os
 
 import numpy as np
 import torch
@@ -67,6 +68,173 @@ def activate(ctx):
         _CTX = prev
 
 
+class _DevPtr:
+    """Zero-copy torch view of raw device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                          "version": 3}
+
+
+def _view(ptr: int, nbytes: int, dtype: torch.dtype, shape) -> torch.Tensor:
+    t = torch.as_tensor(_DevPtr(ptr, nbytes), device=_lib.device())
+    return t.view(dtype).view(shape)
+
+
+class _PeerWork:
+    """Completion of one peer exchange: wait() makes the current stream wait
+    for the senders' epoch flags (cuStreamWaitValue64, no host round trip)."""
+
+    def __init__(self, mesh, flags):
+        self.mesh = mesh
+        self.flags = flags          # [(local flag address, epoch)]
+
+    def wait(self) -> None:
+        st = _lib.stream()
+        for addr, e in self.flags:
+            _lib.check(self.mesh.lib.vr_peer_wait(addr, e, st), "vr_peer_wait")
+
+
+class PeerMesh:
+    """Peer-memory transport of one SlabContext (csrc/peer.cu): symmetric
+    IPC-mapped receive buffers on every rank, copy-engine copies on a side
+    stream, and per-(source, channel) uint64 epoch flags in the receiver's
+    memory (written by the sender behind its data, awaited on the receiver's
+    stream).  Replaces NCCL for the ghost planes and the spectral transposes;
+    NCCL keeps the scalar allreduces.  Buffer creation and growth are
+    collective (every rank makes the same calls in the same order)."""
+
+    GHOST_LO, GHOST_HI, A2A = 0, 1, 2
+    NCH = 4
+
+    def __init__(self, ctx):
+        import ctypes as C
+        self.C = C
+        self.ctx = ctx
+        self.lib = _lib.lib()
+        self.P, self.me = ctx.world, ctx.rank
+        self.hbytes = int(self.lib.vr_peer_handle_bytes())
+        self.side = torch.cuda.Stream()
+        self.epoch = {}
+        self.bufs = {}                   # name -> (local ptr, [ptr on rank q], nbytes)
+        self._opened = []
+        self.flags, self.flags_remote = self._symmetric(self.P * self.NCH * 8)
+
+    # ---- symmetric buffers --------------------------------------------------------
+    def _symmetric(self, nbytes: int):
+        C = self.C
+        ptr = C.c_void_p()
+        handle = C.create_string_buffer(self.hbytes)
+        _lib.check(self.lib.vr_peer_malloc(int(nbytes), C.byref(ptr), handle), "vr_peer_malloc")
+        handles = [None] * self.P
+        tdist.all_gather_object(handles, bytes(handle.raw), group=self.ctx.group)
+        remote = []
+        for q in range(self.P):
+            if q == self.me:
+                remote.append(ptr.value)
+                continue
+            rp = C.c_void_p()
+            _lib.check(self.lib.vr_peer_open(C.create_string_buffer(handles[q], self.hbytes), C.byref(rp)),
+                       "vr_peer_open")
+            self._opened.append(rp.value)
+            remote.append(rp.value)
+        return ptr.value, remote
+
+    def buffer(self, name: str, nbytes: int):
+        """(local ptr, per-rank ptrs) of a symmetric buffer of >= nbytes (grown collectively)."""
+        cur = self.bufs.get(name)
+        if cur is None or cur[2] < nbytes:
+            local, remote = self._symmetric(nbytes)
+            self.bufs[name] = (local, remote, nbytes)   # the old mapping stays valid until teardown
+        return self.bufs[name]
+
+    def tensor(self, name: str, dtype: torch.dtype, numel: int) -> torch.Tensor:
+        esz = torch.empty((), dtype=dtype).element_size()
+        local, _, _ = self.buffer(name, numel * esz)
+        return _view(local, numel * esz, dtype, (numel,))
+
+    def remote_of(self, t: torch.Tensor, q: int) -> int:
+        """Address on rank q of the element t[0] of a view into a symmetric buffer."""
+        p = t.data_ptr()
+        for local, remote, nbytes in self.bufs.values():
+            if local <= p < local + nbytes:
+                return remote[q] + (p - local)
+        raise ValueError("tensor does not live in a symmetric peer buffer")
+
+    def _flag_local(self, src: int, ch: int) -> int:
+        return self.flags + (src * self.NCH + ch) * 8
+
+    def _flag_remote(self, q: int, src: int, ch: int) -> int:
+        return self.flags_remote[q] + (src * self.NCH + ch) * 8
+
+    def _next(self, key: str) -> int:
+        e = self.epoch.get(key, 0) + 1
+        self.epoch[key] = e
+        return e
+
+    def _on_side(self, *tensors):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        for t in tensors:
+            t.record_stream(self.side)
+
+    # ---- ghost planes ---------------------------------------------------------------
+    def ghosts_post(self, x: torch.Tensor, w: int) -> tuple:
+        """Copy-engine ghost exchange of x (..., L1, N2, N3): my first w planes
+        into the left neighbour's hi ghost block, my last w planes into the right
+        neighbour's lo block (double-buffered by epoch parity)."""
+        L1, n2, n3 = x.shape[-3:]
+        lead = tuple(x.shape[:-3])
+        ncomp = int(np.prod(lead)) if lead else 1
+        plane = n2 * n3 * x.element_size()
+        blk = ncomp * w * plane
+        xs = x.reshape((ncomp, L1, n2, n3))
+        if not xs.is_contiguous():
+            xs = xs.contiguous()
+        local, remote, cap = self.buffer("ghost", 4 * blk)
+        cap //= 4
+        e = self._next("ghost")
+        par = e % 2
+        off_lo, off_hi = (2 * par) * cap, (2 * par + 1) * cap
+        left, right = self.ctx.left, self.ctx.right
+        self._on_side(xs)
+        st = self.side.cuda_stream
+        base = xs.data_ptr()
+        cstride = L1 * plane
+        for c in range(ncomp):
+            src_first = base + c * cstride                 # planes [0, w)
+            src_last = base + c * cstride + (L1 - w) * plane
+            _lib.check(self.lib.vr_peer_copy(remote[left] + off_hi + c * w * plane, src_first, w * plane, st),
+                       "vr_peer_copy")
+            _lib.check(self.lib.vr_peer_copy(remote[right] + off_lo + c * w * plane, src_last, w * plane, st),
+                       "vr_peer_copy")
+        _lib.check(self.lib.vr_peer_signal(self._flag_remote(left, self.me, self.GHOST_HI), e, st), "vr_peer_signal")
+        _lib.check(self.lib.vr_peer_signal(self._flag_remote(right, self.me, self.GHOST_LO), e, st), "vr_peer_signal")
+        shape = lead + (w, n2, n3)
+        lo = _view(local + off_lo, blk, x.dtype, shape)
+        hi = _view(local + off_hi, blk, x.dtype, shape)
+        work = _PeerWork(self, [(self._flag_local(left, self.GHOST_LO), e),
+                                (self._flag_local(right, self.GHOST_HI), e)])
+        return lo, hi, [work]
+
+    # ---- all-to-all ------------------------------------------------------------------
+    def alltoall_post(self, out: torch.Tensor, inp: torch.Tensor) -> _PeerWork:
+        """Equal-split all-to-all of flat views: block q of `inp` lands in rank
+        q's `out` (a symmetric buffer view) at block `me`."""
+        nb = inp.numel() * inp.element_size() // self.P
+        self._on_side(inp)
+        st = self.side.cuda_stream
+        e = self._next("a2a")
+        base = inp.data_ptr()
+        for k in range(self.P):
+            q = (self.me + k) % self.P                     # stagger the destinations
+            _lib.check(self.lib.vr_peer_copy(self.remote_of(out, q) + self.me * nb, base + q * nb, nb, st),
+                       "vr_peer_copy")
+            _lib.check(self.lib.vr_peer_signal(self._flag_remote(q, self.me, self.A2A), e, st), "vr_peer_signal")
+        return _PeerWork(self, [(self._flag_local(q, self.A2A), e) for q in range(self.P)])
+
+
 class SlabContext:
     """Decomposition of a global (N1, N2, N3) lattice into x1 slabs."""
 
@@ -84,6 +252,15 @@ class SlabContext:
         self.local_dims = (self.L1, n2, n3)
         self.left = (self.rank - 1) % self.world
         self.right = (self.rank + 1) % self.world
+        self._mesh = None
+
+    @property
+    def mesh(self):
+        """PeerMesh for NCCL (GPU) groups with > 1 rank unless VR_PEER=0; None otherwise."""
+        if self._mesh is None and self.world > 1 and os.environ.get("VR_PEER", "1") != "0" \
+                and tdist.get_backend(self.group) == "nccl":
+            self._mesh = PeerMesh(self)
+        return self._mesh
 
     # ---- collectives on small host arrays ---------------------------------------
     def _dev(self):
@@ -135,6 +312,8 @@ class SlabContext:
         send_hi = x[..., L1 - w:, :, :]
         if self.world == 1:
             return send_hi.contiguous(), send_lo.contiguous(), []
+        if self.mesh is not None:
+            return self.mesh.ghosts_post(x, w)
         send_lo = send_lo.contiguous()
         send_hi = send_hi.contiguous()
         hi = torch.empty_like(send_lo)        # <- right neighbour's first planes
@@ -162,11 +341,32 @@ class SlabContext:
         if self.world == 1:
             out.copy_(inp)
             return None
+        if self.mesh is not None and self._symmetric_view(out):
+            with _lib.timed("dist.alltoall"):
+                work = self.mesh.alltoall_post(out, inp)
+                if async_op:
+                    return work
+                work.wait()
+            return None
         if async_op:
             return tdist.all_to_all_single(out, inp, group=self.group, async_op=True)
         with _lib.timed("dist.alltoall"):
             tdist.all_to_all_single(out, inp, group=self.group)
         return None
+
+    def _symmetric_view(self, t: torch.Tensor) -> bool:
+        try:
+            self.mesh.remote_of(t, self.rank)
+            return True
+        except ValueError:
+            return False
+
+    def buffer(self, name: str, dtype: torch.dtype, numel: int) -> torch.Tensor:
+        """A receive buffer other ranks can write into (symmetric peer buffer
+        when the mesh is active, else a plain device tensor)."""
+        if self.mesh is not None:
+            return self.mesh.tensor(name, dtype, numel)
+        return torch.empty(numel, dtype=dtype, device=_lib.device())
 
     # ---- synthetic-input helpers -------------------------------------------------
     def local_coords(self) -> np.ndarray:
