@@ -254,6 +254,23 @@ int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_globa
 int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
                      void* stream);
 
+/* Peer variants (multi-GPU over NVLink; dist.py PeerMesh): the transposes are
+ * fused into the passes.  vr_dspec_forward_peer stores Y-pass row j straight
+ * into rank j / L2's receive buffer dst[j / L2] (block `me`);
+ * vr_dspec_xpass_peer stores x1 block p into rank p's inverse receive buffer
+ * dst[p]; vr_dspec_inverse_peer reads this rank's blocked inverse receive
+ * buffer directly (no unpack pass).  `dst` is a HOST array of nranks device
+ * pointers (IPC mappings); nranks a power of two <= 8, N2 = 256 on the slab
+ * plan (VR_ERR_UNSUPPORTED otherwise: use the packed NCCL / copy path).  The
+ * caller signals completion (vr_peer_signal) after each producing call. */
+int vr_dspec_forward_peer(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, int me,
+                          void* const* dst, void* stream);
+int vr_dspec_xpass_peer(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
+                        double sigma, double alpha, int64_t n_global, int j0, int n2_global, int l1, const void* recv,
+                        int nranks, int me, void* const* dst, void* stream);
+int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add,
+                          float* out, void* stream);
+
 /* ---- peer-memory transport (multi-GPU, one process per GPU; dist.py) ---------
  * Symmetric buffers: vr_peer_malloc allocates (zeroed) device memory and
  * returns its CUDA IPC handle (vr_peer_handle_bytes() bytes, host memory);

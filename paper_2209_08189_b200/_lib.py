@@ -78,6 +78,10 @@ _SIGS = {
     "vr_dspec_xpass": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _i32, _p, _p, _p],
     "vr_dspec_h1_partial": [_p, _p, _i32, _i32, _i32, _f64, _p, _p],
     "vr_dspec_inverse": [_p, _p, _i32, _i32, _p, _p, _p],
+    "vr_dspec_forward_peer": [_p, _p, _i32, _i32, _i32, _i32, _p, _p],
+    "vr_dspec_xpass_peer": [_p, _i32, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i64, _i32, _i32, _i32, _p, _i32,
+                            _i32, _p, _p],
+    "vr_dspec_inverse_peer": [_p, _p, _i32, _i32, _p, _p, _p],
     # peer-memory transport
     "vr_peer_malloc": [_i64, C.POINTER(_p), _p],
     "vr_peer_free": [_p],
@@ -105,6 +109,7 @@ class NativeError(VelregError):
 # kernels launched per C-ABI call (for the bench's gpu_launches accounting)
 LAUNCHES = {"vr_spec_apply_launches": 0, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
+            "vr_dspec_forward_peer": 2, "vr_dspec_xpass_peer": 1, "vr_dspec_inverse_peer": 2,
             "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
             "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0,

@@ -215,6 +215,18 @@ struct SpecOp {
     const int p = i / xblk;
     return ((int64_t)(p * ncomp + c) * xblk + (i - p * xblk)) * lstride;
   }
+  // distributed X pass with peer output (spectral transposes over NVLink):
+  // block p (x1 rows [p xblk, (p+1) xblk)) is stored straight into rank p's
+  // receive buffer pdst[p] at the sender's block `me` ([me][c][il][jl][kz]).
+  void* pdst[8] = {};
+  int me = 0;
+  __device__ __forceinline__ float2* out_at(float2* T, int c, int i, int64_t lstride, int64_t rowoff) const {
+    const int p = i / xblk;
+    if (pdst[0])
+      return reinterpret_cast<float2*>(pdst[p]) + ((int64_t)(me * ncomp + c) * xblk + (i - p * xblk)) * lstride +
+             rowoff;
+    return T + xoff(c, i, lstride) + rowoff;
+  }
 };
 
 __device__ __forceinline__ int signed_freq(int m, int n) { return m < n / 2 ? m : m - n; }  // fftfreq*n
@@ -434,13 +446,12 @@ __global__ void __launch_bounds__(256) x_op_kernel(const double2* __restrict__ S
   }
   __syncthreads();
   double2* out = line_fft<double2>(res, other, ls, NC * B, rp, tw_s, true);
-  float2* tbase = T + (int64_t)j * n3h + kz0;
   for (int t = threadIdx.x; t < NC * L * nb; t += blockDim.x) {
     const int c = t / (L * nb);
     const int r = t - c * L * nb;
     const int i = r / nb, q = r - i * nb;
     const double2 v = out[(c * B + q) * ls + i];
-    tbase[op.xoff(c, i, lstride) + q] = make_float2((float)v.x, (float)v.y);
+    *op.out_at(T, c, i, lstride, (int64_t)j * n3h + kz0 + q) = make_float2((float)v.x, (float)v.y);
   }
 }
 
@@ -829,6 +840,37 @@ static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_
   return VR_OK;
 }
 
+// Z forward pass only (fast path) into p->S
+static void spec_forward_z(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s, bool f64) {
+  const Dims& d = p->d;
+  const int nrows = d.n1 * d.n2;
+  const int M = d.n3 / 2;
+#define L_Z(MM)                                                                                            \
+  {                                                                                                        \
+    const dim3 g((nrows + (int)fast_lines<MM>() - 1) / (int)fast_lines<MM>(), ncomp);                     \
+    if (f64)                                                                                               \
+      fast::zfwd_fast<MM, double2><<<g, 256, sm_z(MM, 16), s>>>(in, nrows, d.n(), p->nspec, p->stw3h, p->tw3, \
+                                                                p->S);                                     \
+    else                                                                                                   \
+      fast::zfwd_fast<MM, float2><<<g, 256, sm_z(MM, 8), s>>>(in, nrows, d.n(), p->nspec, p->stw3h, p->tw3,  \
+                                                              reinterpret_cast<float2*>(p->S));            \
+  }
+  VR_POW2_SWITCH(M, L_Z)
+#undef L_Z
+}
+
+// Z inverse pass only (fast path): p->T -> out (+ add)
+static void spec_inverse_z(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
+  const Dims& d = p->d;
+  const int nrows = d.n1 * d.n2;
+  const int M = d.n3 / 2;
+#define L_ZI(MM)                                                                                          \
+  fast::zinv_fast<MM><<<dim3((nrows + (int)fast_lines<MM>() - 1) / (int)fast_lines<MM>(), ncomp), 256,    \
+                        sm_zi(MM), s>>>(p->T, nrows, d.n(), p->nspec, p->stw3h, p->tw3, out, add);
+  VR_POW2_SWITCH(M, L_ZI)
+#undef L_ZI
+}
+
 static void spec_inverse_yz(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
   const Dims& d = p->d;
   launch_axis<float2>(p, p->T, 2, ncomp, 1, s);
@@ -1206,6 +1248,84 @@ int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nran
   rowmove_kernel<float2, false><<<(unsigned)((ncomp * pl->d.n1 * pl->d.n2 + 7) / 8), 256, 0, s>>>(
       reinterpret_cast<const float2*>(recv_inv), pl->T, ncomp, pl->d.n1, pl->d.n2, pl->n3h, nranks);
   spec_inverse_yz(pl, ncomp, add, out, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// ---- peer variants: the transposes fused into the x2 / x1 passes (NVLink stores) ----
+static bool peer_ok(const vr_spec_plan* pl, int nranks) {
+  return pl && pl->fast && g_fft_mode && pl->d.n2 == 256 && nranks >= 1 && nranks <= 8 &&
+         (nranks & (nranks - 1)) == 0;
+}
+
+static int log2i(int x) {
+  int s = 0;
+  while ((1 << s) < x) ++s;
+  return s;
+}
+
+// Z + Y forward of `in`; the Y pass stores row j straight into rank j / L2's
+// receive buffer dst[j / L2] (host array of device pointers) at block `me`.
+int vr_dspec_forward_peer(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, int me,
+                          void* const* dst, void* stream) {
+  if (!in || !dst || (ncomp != 1 && ncomp != 3) || me < 0 || me >= nranks) return VR_ERR_ARG;
+  if (!peer_ok(pl, nranks)) return VR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  spec_forward_z(pl, in, ncomp, s, f64 != 0);
+  fs::X2Peer pe{};
+  for (int r = 0; r < nranks; ++r) pe.dst[r] = dst[r];
+  pe.me = me;
+  pe.l2shift = log2i(nranks);
+  pe.ncomp = ncomp;
+  const int nchunks = (pl->n3h + 15) / 16;
+  const dim3 g(pl->d.n1 * nchunks, ncomp);
+  if (f64) {
+    const size_t sm = sizeof(double2) * 16 * fs::line_smem<16>();
+    smem_optin(fs::axis256_dist<double2, false>, sm);
+    fs::axis256_dist<double2, false><<<g, 256, sm, s>>>(pl->S, nullptr, pe, pl->d.n1, pl->n3h, pl->tw2);
+  } else {
+    const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
+    smem_optin(fs::axis256_dist<float2, false>, sm);
+    fs::axis256_dist<float2, false><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(pl->S), nullptr, pe,
+                                                       pl->d.n1, pl->n3h, pl->tw2);
+  }
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// X pass on the transposed block with its output stored straight into rank
+// p's inverse receive buffer dst[p] (block `me`); arguments as vr_dspec_xpass.
+int vr_dspec_xpass_peer(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v, double beta_w, double shift,
+                        double sigma, double alpha, int64_t n_global, int j0, int n2_global, int l1, const void* recv,
+                        int nranks, int me, void* const* dst, void* stream) {
+  if (!px || !recv || !dst || (ncomp != 1 && ncomp != 3) || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
+  if (nranks < 1 || nranks > 8 || me < 0 || me >= nranks || px->d.n1 / l1 != nranks) return VR_ERR_ARG;
+  if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
+  if (!px->fast) return VR_ERR_UNSUPPORTED;
+  if (ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;
+  SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
+  for (int p = 0; p < nranks; ++p) op.pdst[p] = dst[p];
+  op.me = me;
+  spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, nullptr);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// inverse: Y inverse reading the blocked receive buffer (unpack fused), Z inverse -> out (+ add)
+int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add,
+                          float* out, void* stream) {
+  if (!recv_inv || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
+  if (!peer_ok(pl, nranks)) return VR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  fs::X2Peer pe{};
+  pe.l2shift = log2i(nranks);
+  pe.ncomp = ncomp;
+  const int nchunks = (pl->n3h + 15) / 16;
+  const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
+  smem_optin(fs::axis256_dist<float2, true>, sm);
+  fs::axis256_dist<float2, true><<<dim3(pl->d.n1 * nchunks, ncomp), 256, sm, s>>>(
+      reinterpret_cast<const float2*>(recv_inv), pl->T, pe, pl->d.n1, pl->n3h, pl->tw2);
+  spec_inverse_z(pl, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }

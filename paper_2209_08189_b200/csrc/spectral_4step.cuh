@@ -209,9 +209,9 @@ __global__ void __launch_bounds__(3 * XB * 16, (sizeof(CF) == 8 ? 20 : 12) / XB)
   float2* fline = reinterpret_cast<float2*>(fs_smem) + (c * XB + q) * LS;
   line_fft<float2, R2>(w, t, fline, tw, true);
   if (ok) {
-    float2* tb = T + (int64_t)j * n3h + kz0 + q;
+    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) tb[op.xoff(c, out_freq<R2>(t, u), lstride)] = w[u];
+    for (int u = 0; u < 16; ++u) *op.out_at(T, c, out_freq<R2>(t, u), lstride, rowoff) = w[u];
   }
 }
 
@@ -263,10 +263,60 @@ __global__ void __launch_bounds__(256, sizeof(CF) == 8 ? 3 : 2) xdiag256(const C
   __syncthreads();   // transpose scratch reused by the inverse
   line_fft<float2, R2>(w, t, reinterpret_cast<float2*>(fs_smem) + q * line_smem<R2>(), tw, true);
   if (ok) {
-    float2* tb = T + (int64_t)j * n3h + kz0 + q;
+    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) tb[op.xoff(c, out_freq<R2>(t, u), lstride)] = w[u];
+    for (int u = 0; u < 16; ++u) *op.out_at(T, c, out_freq<R2>(t, u), lstride, rowoff) = w[u];
   }
+}
+
+// ---- distributed x2 passes with the transpose fused in (L = n2 = 256) -------
+// Between the slab layout [c][i][j][kz] and the rank-blocked transpose layout
+// [r][c][i][jl][kz] (j = r L2 + jl, r = the x2 block's owner):
+//   forward (INV = false): x2 FFT of the slab spectrum `in`; output row j is
+//     stored straight into rank r = j / L2's receive buffer dst[r] at the
+//     sender's block `me` (NVLink stores: pack + all-to-all are this kernel's
+//     epilogue);
+//   inverse (INV = true): rows loaded from this rank's receive buffer `in` in
+//     the blocked layout (unpack fused into the loads), x2 inverse FFT, stored
+//     to the slab spectrum `out`.
+struct X2Peer {
+  void* dst[8];
+  int me, l2shift, ncomp;
+};
+
+template <typename C, bool INV>
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(const C* __restrict__ in,
+                                                                          C* __restrict__ out, X2Peer pe, int L1,
+                                                                          int n3h, const double2* __restrict__ tw) {
+  constexpr int R2 = 16, NB = 16, N2 = 256;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  C* smem = reinterpret_cast<C*>(fs_smem);
+  const int q = threadIdx.x % NB, t = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int i = blockIdx.x / nchunks, kz0 = (blockIdx.x - i * nchunks) * NB, c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
+  const int L2 = N2 >> pe.l2shift;
+  auto slab_off = [&](int j) -> int64_t { return (((int64_t)c * L1 + i) * N2 + j) * n3h + kz0 + q; };
+  auto blk_off = [&](int r, int jl) -> int64_t {
+    return ((((int64_t)r * pe.ncomp + c) * L1 + i) * L2 + jl) * n3h + kz0 + q;
+  };
+  C v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int j = t + R2 * m;
+    if (ok) v[m] = INV ? in[blk_off(j >> pe.l2shift, j & (L2 - 1))] : in[slab_off(j)];
+    else { v[m].x = 0; v[m].y = 0; }
+  }
+  line_fft<C, R2>(v, t, smem + q * line_smem<R2>(), tw, INV);
+  if (ok) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int j = out_freq<R2>(t, u);
+      if (INV) out[slab_off(j)] = v[u];
+      else reinterpret_cast<C*>(pe.dst[j >> pe.l2shift])[blk_off(pe.me, j & (L2 - 1))] = v[u];
+    }
+  }
+  if (!INV) __threadfence_system();   // peer stores visible before the completion flag
 }
 
 }  // namespace fs

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(NC == 3 ? 384 : 256, NC == 3 ? 2 : 3) xop_fast
     __syncthreads();
     fft_tile<CF, L, true>(tile, tw_s);
     __syncthreads();
-    float2* tbase = T + (int64_t)j * n3h + kz0;
+
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = threadIdx.x + u * NT;
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NC == 3 ? 384 : 256, NC == 3 ? 2 : 3) xop_fast
       const int c = ci / L, i = ci - c * L;
       if (q < nb) {
         const CF v = tile[(c * B + q) * PL + padi(i)];
-        tbase[op.xoff(c, i, lstride) + q] = make_float2((float)v.x, (float)v.y);
+        *op.out_at(T, c, i, lstride, (int64_t)j * n3h + kz0 + q) = make_float2((float)v.x, (float)v.y);
       }
     }
   }

@@ -10,6 +10,7 @@ callers (SPEC.md:175).
 """
 from __future__ import annotations
 
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -115,6 +116,77 @@ class DistSpectralWorkspace:
         self.irecv = ctx.buffer(f"spec_irecv_{n1}x{n2}x{n3}", torch.float32, 2 * nc)
         self.per_comp = ctx.L1 * n2 * self.n3h   # complex elements per component
         self.device = torch.cuda.current_device()
+        # transposes fused into the passes over peer memory (csrc/spectral.cu
+        # vr_dspec_*_peer) when the peer mesh is active and the shapes allow
+        P = ctx.world
+        self.peer = (ctx.mesh is not None and n2 == 256 and 1 < P <= 8 and (P & (P - 1)) == 0
+                     and os.environ.get("VR_PEER_FUSED", "1") != "0")
+        self._dst_cache = {}
+
+    # ---- peer (fused-transpose) path ---------------------------------------------
+    def _dst(self, view: torch.Tensor):
+        """Host array of the P device addresses of `view` (a symmetric buffer region)."""
+        key = view.data_ptr()
+        arr = self._dst_cache.get(key)
+        if arr is None:
+            mesh = self.ctx.mesh
+            arr = (C.c_void_p * self.ctx.world)(*[mesh.remote_of(view, q) for q in range(self.ctx.world)])
+            self._dst_cache[key] = arr
+        return arr
+
+    def _signal(self) -> int:
+        mesh, st = self.ctx.mesh, _lib.stream()
+        e = mesh._next("a2a")
+        for q in range(self.ctx.world):
+            _lib.check(mesh.lib.vr_peer_signal(mesh._flag_remote(q, self.ctx.rank, mesh.A2A), e, st),
+                       "vr_peer_signal")
+        return e
+
+    def _wait(self, e: int) -> None:
+        mesh, st = self.ctx.mesh, _lib.stream()
+        for q in range(self.ctx.world):
+            _lib.check(mesh.lib.vr_peer_wait(mesh._flag_local(q, mesh.A2A), e, st), "vr_peer_wait")
+
+    def _regions(self, c: int, ncomp: int, f64: bool):
+        """(recv, irecv) views of component c's regions (or all ncomp from 0)."""
+        rv = self.recv if f64 else self.recv.view(torch.float32)   # 2 reals per complex either way
+        off, n = c * self.per_comp * 2, self.per_comp * 2 * ncomp
+        return rv[off:off + n], self.irecv[off:off + n]
+
+    def _apply_peer(self, kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha, comps) -> bool:
+        lib, st, ctx = _lib.lib(), _lib.stream(), self.ctx
+        P, me = ctx.world, ctx.rank
+        n1, n2, n3 = self.grid.dims
+        nvox = x[0].numel() if x.dim() == 4 else x.numel()
+        groups = [(c, 1) for c in range(3)] if comps == "pipelined" else [(0, 3 if x.dim() == 4 else 1)]
+        ef, ei = [], []
+        with _lib.timed("dist.spectral"):
+            for c, nc in groups:
+                rv, _ = self._regions(c, nc, f64)
+                rc = lib.vr_dspec_forward_peer(self._pl, x.data_ptr() + 4 * c * nvox, nc, int(f64), P, me,
+                                               self._dst(rv), st)
+                if rc == -5:
+                    if ef:
+                        raise RuntimeError("fused-transpose path became unsupported mid-operator")
+                    self.peer = False
+                    return False
+                _lib.check(rc, "vr_dspec_forward_peer")
+                ef.append(self._signal())
+            for (c, nc), e in zip(groups, ef):
+                rv, iv = self._regions(c, nc, f64)
+                self._wait(e)
+                _lib.check(lib.vr_dspec_xpass_peer(self._px, int(kind), nc, int(f64), float(beta_v), float(beta_w),
+                                                   float(shift), float(sigma), float(alpha), n1 * n2 * n3,
+                                                   ctx.rank * ctx.L2, n2, ctx.L1, rv.data_ptr(), P, me,
+                                                   self._dst(iv), st), "vr_dspec_xpass_peer")
+                ei.append(self._signal())
+            for (c, nc), e in zip(groups, ei):
+                _, iv = self._regions(c, nc, f64)
+                self._wait(e)
+                a = None if add is None else add.data_ptr() + 4 * c * nvox
+                _lib.check(lib.vr_dspec_inverse_peer(self._pl, iv.data_ptr(), nc, P, a, out.data_ptr() + 4 * c * nvox,
+                                                     st), "vr_dspec_inverse_peer")
+        return True
 
     def _exchange(self, dst: torch.Tensor, src: torch.Tensor, ncomp: int, cplx_words: int) -> None:
         """One all-to-all for all components: blocks are [rank][component][...]."""
@@ -131,6 +203,10 @@ class DistSpectralWorkspace:
             out = torch.empty_like(x)
         f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2)
         P = self.ctx.world
+        if self.peer:
+            comps = "pipelined" if (ncomp == 3 and kind != _lib.SPEC_K) else "fused"
+            if self._apply_peer(kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha, comps):
+                return out
         if ncomp == 3 and kind != _lib.SPEC_K and P > 1:
             return self._apply_pipelined(kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha)
         _lib.check(lib.vr_dspec_forward(self._pl, x.data_ptr(), ncomp, int(f64), P, self.send.data_ptr(), st),
@@ -204,9 +280,19 @@ class DistSpectralWorkspace:
         lib = _lib.lib()
         st = _lib.stream()
         P = self.ctx.world
-        _lib.check(lib.vr_dspec_forward(self._pl, f.data_ptr(), 1, 1, P, self.send.data_ptr(), st),
-                   "vr_dspec_forward")
-        self._exchange(self.recv, self.send, 1, 2)
+        done = False
+        if self.peer:
+            rv, _ = self._regions(0, 1, True)
+            rc = lib.vr_dspec_forward_peer(self._pl, f.data_ptr(), 1, 1, P, self.ctx.rank, self._dst(rv), st)
+            if rc == 0:
+                self._wait(self._signal())
+                done = True
+            elif rc != -5:
+                _lib.check(rc, "vr_dspec_forward_peer")
+        if not done:
+            _lib.check(lib.vr_dspec_forward(self._pl, f.data_ptr(), 1, 1, P, self.send.data_ptr(), st),
+                       "vr_dspec_forward")
+            self._exchange(self.recv, self.send, 1, 2)
         n = float(np.prod(self.grid.dims))
         out = _lib.out_buf(1)
         _lib.check(lib.vr_dspec_h1_partial(self._px, self.recv.data_ptr(), self.ctx.rank * self.ctx.L2,

@@ -23,6 +23,11 @@ from .grid import Grid, ScalarField, VectorField, TWO_PI
 
 INTERP_ORDERS = ("linear", "cubic")
 
+# slab sweeps with peer-memory ghosts: 0 = exchange, then one full-slab launch
+# (default); 1 = interior planes overlap the exchange, boundary planes after
+import os as _os
+_SWEEP_SPLIT = int(_os.environ.get("VR_SWEEP_SPLIT", "0"))
+
 
 @dataclass
 class TransportConfig:
@@ -208,7 +213,12 @@ class TransportOperators:
         L1 = ctx.local_dims[0]
         with _lib.timed("dist.sweep"):
             lo, hi, works = ctx.ghosts_async(values, w)
-            if L1 > 2 * w:
+            if ctx.mesh is not None and _SWEEP_SPLIT == 0:
+                # copy-engine ghosts land in ~10 us: wait, then ONE full-slab launch
+                # (the interior / boundary split costs two extra launch tails)
+                ctx.finish(works)
+                launch(lo, hi, 0, L1)
+            elif L1 > 2 * w:
                 launch(lo, hi, w, L1 - 2 * w)
                 ctx.finish(works)
                 launch(lo, hi, 0, w)
