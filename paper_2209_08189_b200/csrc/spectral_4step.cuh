@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
   const int nchunks = (n3h + NB - 1) / NB;
   const int i = blockIdx.x / nchunks, kz0 = (blockIdx.x - i * nchunks) * NB, c = blockIdx.y;
   const bool ok = kz0 + q < n3h;
-  const int L2 = N2 >> pe.l2shift;
+  const int L2 = N2 >> pe.l2shift, jshift = 8 - pe.l2shift;   // row j -> (r, jl) = (j >> jshift, j & (L2-1))
   auto slab_off = [&](int j) -> int64_t { return (((int64_t)c * L1 + i) * N2 + j) * n3h + kz0 + q; };
   auto blk_off = [&](int r, int jl) -> int64_t {
     return ((((int64_t)r * pe.ncomp + c) * L1 + i) * L2 + jl) * n3h + kz0 + q;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
     const int j = t + R2 * m;
-    if (ok) v[m] = INV ? in[blk_off(j >> pe.l2shift, j & (L2 - 1))] : in[slab_off(j)];
+    if (ok) v[m] = INV ? in[blk_off(j >> jshift, j & (L2 - 1))] : in[slab_off(j)];
     else { v[m].x = 0; v[m].y = 0; }
   }
   line_fft<C, R2>(v, t, smem + q * line_smem<R2>(), tw, INV);
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
     for (int u = 0; u < 16; ++u) {
       const int j = out_freq<R2>(t, u);
       if (INV) out[slab_off(j)] = v[u];
-      else reinterpret_cast<C*>(pe.dst[j >> pe.l2shift])[blk_off(pe.me, j & (L2 - 1))] = v[u];
+      else reinterpret_cast<C*>(pe.dst[j >> jshift])[blk_off(pe.me, j & (L2 - 1))] = v[u];
     }
   }
   if (!INV) __threadfence_system();   // peer stores visible before the completion flag
