@@ -287,6 +287,11 @@ int vr_peer_handle_bytes(void);
 int vr_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
 int vr_peer_signal(unsigned long long* flag, unsigned long long value, void* stream);
 int vr_peer_wait(const unsigned long long* flag, unsigned long long value, void* stream);
+/* ghost planes of a float slab src (ncomp, L1, N2, N3): planes [0, w) of every
+ * component -> left_hi (ncomp, w, N2, N3), planes [L1-w, L1) -> right_lo;
+ * plane = N2*N3 (multiple of 4), 16-byte-aligned (peer-mapped) pointers. */
+int vr_peer_halo_put(const float* src, int ncomp, int L1, int64_t plane, int w, float* left_hi, float* right_lo,
+                     void* stream);
 
 #ifdef __cplusplus
 }

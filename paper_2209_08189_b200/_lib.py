@@ -91,6 +91,7 @@ _SIGS = {
     "vr_peer_copy": [_p, _p, _i64, _p],
     "vr_peer_signal": [_p, C.c_uint64, _p],
     "vr_peer_wait": [_p, C.c_uint64, _p],
+    "vr_peer_halo_put": [_p, _i32, _i32, _i64, _i32, _p, _p, _p],
 }
 
 EXPORTED = tuple(_SIGS)

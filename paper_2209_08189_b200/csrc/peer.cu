@@ -20,6 +20,7 @@
 // after a later exchange with the same peer has completed.
 #include <cuda.h>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include "common.cuh"
 #include "../../include/velreg_b200.h"
@@ -48,9 +49,42 @@ __global__ void signal_kernel(unsigned long long* flag, unsigned long long value
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
 
+// Ghost-plane put: the first w planes of every component go to the left
+// neighbour's hi ghost block, the last w planes to the right neighbour's lo
+// block (both IPC-mapped), one float4 per thread per step.  An SM copy: a
+// copy-engine copy of these 1-3 MB blocks costs ~12 us of launch latency each.
+__global__ void __launch_bounds__(256) halo_put_kernel(const float4* __restrict__ src, int ncomp, int64_t cstride4,
+                                                       int64_t plane4, int L1, int w, float4* __restrict__ left_hi,
+                                                       float4* __restrict__ right_lo) {
+  const int64_t blk4 = (int64_t)w * plane4;          // float4s per component block
+  const int64_t n = 2 * ncomp * blk4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t side = e / (ncomp * blk4), r = e - side * ncomp * blk4;
+    const int64_t c = r / blk4, o = r - c * blk4;
+    if (side == 0) left_hi[c * blk4 + o] = src[c * cstride4 + o];
+    else right_lo[c * blk4 + o] = src[c * cstride4 + (int64_t)(L1 - w) * plane4 + o];
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+// ghost planes of a (ncomp, L1, N2, N3) float slab into the neighbours' blocks
+// (ncomp, w, N2, N3); plane = N2 * N3 (a multiple of 4), 16-byte-aligned pointers
+int vr_peer_halo_put(const float* src, int ncomp, int L1, int64_t plane, int w, float* left_hi, float* right_lo,
+                     void* stream) {
+  if (!src || !left_hi || !right_lo || ncomp < 1 || w < 1 || w > L1 || plane % 4) return VR_ERR_ARG;
+  if (((uintptr_t)src | (uintptr_t)left_hi | (uintptr_t)right_lo) & 15) return VR_ERR_ARG;
+  const int64_t n4 = 2 * (int64_t)ncomp * w * (plane / 4);
+  const unsigned grid = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+  halo_put_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(src), ncomp, (int64_t)L1 * plane / 4, plane / 4, L1, w,
+      reinterpret_cast<float4*>(left_hi), reinterpret_cast<float4*>(right_lo));
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
 
 int vr_peer_malloc(int64_t bytes, void** ptr, void* handle_out) {
   if (bytes <= 0 || !ptr || !handle_out) return VR_ERR_ARG;

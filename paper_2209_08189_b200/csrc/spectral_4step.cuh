@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
       else reinterpret_cast<C*>(pe.dst[j >> jshift])[blk_off(pe.me, j & (L2 - 1))] = v[u];
     }
   }
-  if (!INV) __threadfence_system();   // peer stores visible before the completion flag
+  // (no per-thread system fence: the completion flag is stored by a kernel
+  // ordered behind this one on the stream, after its own fence.sys -- a
+  // per-thread fence here measured 0.185 vs ~0.12 ms per component)
 }
 
 }  // namespace fs

@@ -193,22 +193,16 @@ class PeerMesh:
         if not xs.is_contiguous():
             xs = xs.contiguous()
         local, remote, cap = self.buffer("ghost", 4 * blk)
-        cap //= 4
+        cap = (cap // 4) & ~255
         e = self._next("ghost")
         par = e % 2
         off_lo, off_hi = (2 * par) * cap, (2 * par + 1) * cap
         left, right = self.ctx.left, self.ctx.right
-        self._on_side(xs)
-        st = self.side.cuda_stream
-        base = xs.data_ptr()
-        cstride = L1 * plane
-        for c in range(ncomp):
-            src_first = base + c * cstride                 # planes [0, w)
-            src_last = base + c * cstride + (L1 - w) * plane
-            _lib.check(self.lib.vr_peer_copy(remote[left] + off_hi + c * w * plane, src_first, w * plane, st),
-                       "vr_peer_copy")
-            _lib.check(self.lib.vr_peer_copy(remote[right] + off_lo + c * w * plane, src_last, w * plane, st),
-                       "vr_peer_copy")
+        # one SM copy kernel on the current stream (ordered behind the producer
+        # of x), then the two completion flags
+        st = _lib.stream()
+        _lib.check(self.lib.vr_peer_halo_put(xs.data_ptr(), ncomp, L1, n2 * n3, w, remote[left] + off_hi,
+                                             remote[right] + off_lo, st), "vr_peer_halo_put")
         _lib.check(self.lib.vr_peer_signal(self._flag_remote(left, self.me, self.GHOST_HI), e, st), "vr_peer_signal")
         _lib.check(self.lib.vr_peer_signal(self._flag_remote(right, self.me, self.GHOST_LO), e, st), "vr_peer_signal")
         shape = lead + (w, n2, n3)
