@@ -922,6 +922,33 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
     }
     return g.x;
   }
+  if (p->fast && g_fft_mode && g_xdiag && !reduce && op.kind != VR_SPEC_K &&
+      (d.n1 == 512 || d.n1 == 1024 || d.n1 == 2048)) {
+    // long x1 lines (the transposed block of a 2 / 4 / 8-rank x1-slab run):
+    // three-step register FFT, one component per grid row
+#define XLONG(R3, NBF, NBD)                                                                                  \
+  {                                                                                                          \
+    if (f64) {                                                                                               \
+      const int nch = (p->n3h + NBD - 1) / NBD;                                                              \
+      const size_t sm = sizeof(double2) * NBD * fs::lf3::smem_elems<R3>();                                   \
+      smem_optin(fs::xdiag_long<double2, R3, NBD>, sm);                                                      \
+      fs::xdiag_long<double2, R3, NBD><<<dim3(d.n2 * nch, nc), NBD * 16 * R3, sm, s>>>(Sd, Tt, d.n2, p->n3h,  \
+                                                                                       p->tw1, op);          \
+      return d.n2 * nch;                                                                                     \
+    } else {                                                                                                 \
+      const int nch = (p->n3h + NBF - 1) / NBF;                                                              \
+      const size_t sm = sizeof(float2) * NBF * fs::lf3::smem_elems<R3>();                                   \
+      smem_optin(fs::xdiag_long<float2, R3, NBF>, sm);                                                       \
+      fs::xdiag_long<float2, R3, NBF><<<dim3(d.n2 * nch, nc), NBF * 16 * R3, sm, s>>>(                       \
+          reinterpret_cast<const float2*>(Sd), Tt, d.n2, p->n3h, p->tw1, op);                                \
+      return d.n2 * nch;                                                                                     \
+    }                                                                                                        \
+  }
+    if (d.n1 == 512) XLONG(2, 16, 8)
+    if (d.n1 == 1024) XLONG(4, 8, 8)
+    XLONG(8, 4, 4)
+#undef XLONG
+  }
   if (p->fast && g_fft_mode && d.n1 == 256 && nc == 3 && !reduce) {
     constexpr int LS = 273;
 #define XOP4(XB)                                                                                             \

@@ -323,3 +323,170 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
 
 }  // namespace fs
 }  // namespace vr
+
+// ---------------------------------------------------------------------------------
+// Three-step register FFT for long lines, L = 16 x 16 x R3 (R3 in {2, 4, 8}:
+// L = 512 / 1024 / 2048 -- the x1 lines of the transposed block in an x1-slab
+// run on 2 / 4 / 8 GPUs).  T = 16 R3 threads per line, 16 values per thread:
+//   forward  x[t + T m] -[DFT-16 over m]-[x W_L^{t k1}]-> transpose 1
+//            -[DFT-16 over t_hi (t = t_lo + R3 t_hi)]-[x W_T^{t_lo k1'}]-> transpose 2
+//            -[DFT-R3 over t_lo]-> X[k1 + 16 (k1' + 16 k2')]
+//   inverse  the same stages run BACKWARD with conjugate twiddles (the DFT is
+//            unitary up to scale: F^H = D1^H W1^H P1^T D2^H W2^H P2^T D3^H), so
+//            the spectrum never needs reordering and the result lands back in
+//            the input layout x[t + T m] (unnormalised, like the other engines).
+// Two shared transposes per transform (the Stockham radix-8 path needs one
+// round trip per stage) and -- with NB lines interleaved per CTA -- 128-B
+// coalesced row segments for the strided x1 lines.
+namespace vr {
+namespace fs {
+namespace lf3 {
+
+template <int R3> __host__ __device__ constexpr int T() { return 16 * R3; }
+// per-line shared elements, odd so that interleaved lines start on distinct banks
+template <int R3> __host__ __device__ constexpr int smem_elems() {
+  return ((16 * R3 * 17) > (256 * (R3 + 1)) ? (16 * R3 * 17) : (256 * (R3 + 1))) | 1;
+}
+
+// in-register DFT of R3 (2 / 4 / 8) values, natural order
+template <typename C, int R>
+__device__ __forceinline__ void dft_r(C (&v)[R], bool inv) {
+  if constexpr (R == 2) {
+    const C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    dft4(v[0], v[1], v[2], v[3], inv);
+  } else {
+    dft8(v, inv);
+  }
+}
+
+template <typename C>
+__device__ __forceinline__ C tw_at(const double2* __restrict__ tw, int idx, bool inv) {
+  double2 w = __ldg(tw + idx);
+  if (inv) w.y = -w.y;
+  return cvt<C>(w);
+}
+
+// pair p = (k1, k1') of stage 3 owned by thread u: p = u + T s, s < 16 / R3
+// forward: v holds x[t + T m] on entry, on exit v[s * R3 + k2'] = X[k1 + 16 (k1' + 16 k2')]
+// twiddles come from the W_L table: W_T^m = W_L^(16 m)
+template <typename C, int R3>
+__device__ __forceinline__ void forward(C (&v)[16], int u, C* sm, const double2* __restrict__ twL) {
+  constexpr int Tn = T<R3>(), L = 256 * R3;
+  dft16(v, false);
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw_at<C>(twL, (u * k1) & (L - 1), false));
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) sm[u * 17 + k1] = v[k1];
+  __syncthreads();
+  {
+    const int k1 = u / R3, tlo = u - (u / R3) * R3;   // stage-2 pair (k1, t_lo)
+#pragma unroll
+    for (int th = 0; th < 16; ++th) v[th] = sm[(tlo + R3 * th) * 17 + k1];
+    dft16(v, false);
+#pragma unroll
+    for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], tw_at<C>(twL, 16 * ((tlo * q) & (Tn - 1)), false));
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sm[(k1 * 16 + q) * (R3 + 1) + tlo] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 16 / R3; ++s) {
+    const int p = u + Tn * s;
+    C r[R3];
+#pragma unroll
+    for (int tl = 0; tl < R3; ++tl) r[tl] = sm[p * (R3 + 1) + tl];
+    dft_r<C, R3>(r, false);
+#pragma unroll
+    for (int k2 = 0; k2 < R3; ++k2) v[s * R3 + k2] = r[k2];
+  }
+}
+
+// frequency of v[s * R3 + k2] after forward (pair p = u + T s = k1 * 16 + k1')
+template <int R3>
+__device__ __forceinline__ int freq(int u, int idx) {
+  const int s = idx / R3, k2 = idx - s * R3;
+  const int p = u + T<R3>() * s, k1 = p >> 4, k1p = p & 15;
+  return k1 + 16 * (k1p + 16 * k2);
+}
+
+// inverse: the forward's stages backward with conjugate twiddles (layouts as
+// produced by forward); on exit v holds x[t + T m] (times L)
+template <typename C, int R3>
+__device__ __forceinline__ void inverse(C (&v)[16], int u, C* sm, const double2* __restrict__ twL) {
+  constexpr int Tn = T<R3>(), L = 256 * R3;
+#pragma unroll
+  for (int s = 0; s < 16 / R3; ++s) {
+    const int p = u + Tn * s;
+    C r[R3];
+#pragma unroll
+    for (int k2 = 0; k2 < R3; ++k2) r[k2] = v[s * R3 + k2];
+    dft_r<C, R3>(r, true);
+#pragma unroll
+    for (int tl = 0; tl < R3; ++tl) sm[p * (R3 + 1) + tl] = r[tl];
+  }
+  __syncthreads();
+  const int k1 = u / R3, tlo = u - (u / R3) * R3;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = sm[(k1 * 16 + q) * (R3 + 1) + tlo];
+#pragma unroll
+  for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], tw_at<C>(twL, 16 * ((tlo * q) & (Tn - 1)), true));
+  dft16(v, true);
+  __syncthreads();
+#pragma unroll
+  for (int th = 0; th < 16; ++th) sm[(tlo + R3 * th) * 17 + k1] = v[th];
+  __syncthreads();
+#pragma unroll
+  for (int k1b = 0; k1b < 16; ++k1b) v[k1b] = sm[u * 17 + k1b];
+#pragma unroll
+  for (int k1b = 1; k1b < 16; ++k1b) v[k1b] = cmul(v[k1b], tw_at<C>(twL, (u * k1b) & (L - 1), true));
+  dft16(v, true);
+}
+
+}  // namespace lf3
+
+// X pass for component-diagonal symbols on long lines (L = 256 R3): NB
+// consecutive kz per CTA (lane = q + NB u), one component per grid row;
+// forward in CF, symbol, inverse in f32 -> T (or the peer destinations).
+template <typename CF, int R3, int NB>
+__global__ void __launch_bounds__(NB * 16 * R3, 1) xdiag_long(const CF* __restrict__ S, float2* __restrict__ T,
+                                                              int n2, int n3h, const double2* __restrict__ twL,
+                                                              SpecOp op) {
+  constexpr int Tn = lf3::T<R3>(), L = 256 * R3, LS = lf3::smem_elems<R3>();
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB;
+  const int c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
+  const int64_t lstride = (int64_t)n2 * n3h;
+  const CF* sb = S + (int64_t)j * n3h + kz0 + q;
+  CF v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (ok) v[m] = sb[op.xoff(c, u + Tn * m, lstride)];
+    else { v[m].x = 0; v[m].y = 0; }
+  }
+  lf3::forward<CF, R3>(v, u, reinterpret_cast<CF*>(fs_smem) + q * LS, twL);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)(kz0 + q);
+  float2 w[16];
+#pragma unroll
+  for (int idx = 0; idx < 16; ++idx) {
+    double2 a = to_d(v[idx]);
+    diag_symbol_at<16>(op, signed_freq(lf3::freq<R3>(u, idx), L), k2, k3, a);
+    w[idx] = make_float2((float)a.x, (float)a.y);
+  }
+  __syncthreads();   // the shared buffer is reused by the f32 inverse
+  lf3::inverse<float2, R3>(w, u, reinterpret_cast<float2*>(fs_smem) + q * LS, twL);
+  if (ok) {
+    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) *op.out_at(T, c, u + Tn * m, lstride, rowoff) = w[m];
+  }
+}
+
+}  // namespace fs
+}  // namespace vr
