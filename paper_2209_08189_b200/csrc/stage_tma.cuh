@@ -32,11 +32,18 @@ constexpr int NT = 128;                 // threads per CTA
 // points), box budget per CTA, CTAs per SM the launch bounds aim for.  (PPT = 2
 // with 24 KB boxes and 9 CTAs / SM measured 6 % slower: the halo share of the
 // box grows faster than residency helps.)
-template <int PPT_> struct Cfg {
+template <int PPT_, int BUDGET_KB = 36, int CTAS = 6, bool PAD32 = true> struct Cfg {
   static constexpr int PPT = PPT_;
-  static constexpr int kSmemBudget = 36 * 1024;
-  static constexpr int kCtas = 6;
+  static constexpr int kSmemBudget = BUDGET_KB * 1024;
+  static constexpr int kCtas = CTAS;
+  // box row pitch: a multiple of 32 floats (PAD32) or the copied length (a
+  // multiple of 4) nudged off multiples of 32 -- a smaller box, more CTAs / SM
+  static constexpr bool kPad32 = PAD32;
 };
+// residency variants (vr_set_gather_mode 1 / 2 / 3)
+using CfgA = Cfg<4, 36, 6, true>;
+using CfgB = Cfg<4, 30, 7, false>;
+using CfgC = Cfg<4, 27, 8, false>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -112,11 +119,12 @@ struct PointSplit {
 // shared-memory latency.)  A box over budget, or a tile with a non-finite or
 // huge displacement, gathers directly.  ORDER: ORDER_CUBIC or ORDER_LINEAR;
 // epi(idx, v) writes voxel idx.
-template <int ORDER, bool SLAB, class Epi, int PPT>
-__global__ void __launch_bounds__(NT, Cfg<PPT>::kCtas) sweep_kernel(PlaneSrc<1, SLAB> src, Dims d,
-                                                                    const float* __restrict__ disp, Tile T, int x0,
-                                                                    Epi epi) {
-  constexpr int kSmemBudget = Cfg<PPT>::kSmemBudget;
+template <int ORDER, bool SLAB, class Epi, class CF>
+__global__ void __launch_bounds__(NT, CF::kCtas) sweep_kernel(PlaneSrc<1, SLAB> src, Dims d,
+                                                              const float* __restrict__ disp, Tile T, int x0,
+                                                              Epi epi) {
+  constexpr int PPT = CF::PPT;
+  constexpr int kSmemBudget = CF::kSmemBudget;
   constexpr int LO = ORDER == ORDER_CUBIC ? 1 : 0;   // stencil reach below / above the base index
   constexpr int HI = ORDER == ORDER_CUBIC ? 2 : 1;
   extern __shared__ __align__(128) float box[];
@@ -180,7 +188,8 @@ __global__ void __launch_bounds__(NT, Cfg<PPT>::kCtas) sweep_kernel(PlaneSrc<1, 
     b.len = ((e1 + HI + 1 - b.s) + 3) & ~3;
     // row pitch a multiple of 32 floats: lanes of a warp split across two box
     // rows / planes still hit disjoint banks
-    b.pitch = (b.len + 31) & ~31;
+    if (CF::kPad32) b.pitch = (b.len + 31) & ~31;
+    else b.pitch = (b.len & 31) == 0 ? b.len + 4 : b.len;
     b.ok = !bb && a0 <= a1 && b.len <= d.n3 && b.ny <= d.n2 && (SLAB || b.nx <= d.n1) &&
            (int64_t)b.nx * b.ny * b.pitch * 4 <= kSmemBudget;
     if (b.ok) mbar_expect_tx(smem_u32(&bar), (unsigned)(b.nx * b.ny * b.len * 4));

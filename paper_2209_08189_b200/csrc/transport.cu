@@ -470,15 +470,23 @@ static int g_gather_mode = 1;
 static bool use_staged(int order, const Dims& d, const float* src, const float* lo = nullptr,
                        const float* hi = nullptr) {
   const uintptr_t a = (uintptr_t)src | (uintptr_t)lo | (uintptr_t)hi;
-  return g_gather_mode == 1 && order == ORDER_CUBIC && stg::staged_ok(d) && (a & 15) == 0;
+  return g_gather_mode >= 1 && order == ORDER_CUBIC && stg::staged_ok(d) && (a & 15) == 0;
+}
+
+template <int ORD, bool SLAB, class Epi, class CF>
+static void launch_staged_cfg(const PlaneSrc<1, SLAB>& ps, const Dims& d, const float* disp, int x0, int nx, Epi epi,
+                              cudaStream_t s) {
+  const stg::Tile T = stg::tile_for(d, CF::PPT);
+  stg::sweep_kernel<ORD, SLAB, Epi, CF><<<stg::sweep_grid(d, T, nx), stg::NT, CF::kSmemBudget, s>>>(ps, d, disp, T,
+                                                                                                 x0, epi);
 }
 
 template <int ORD, bool SLAB, class Epi>
 static void launch_staged(const PlaneSrc<1, SLAB>& ps, const Dims& d, const float* disp, int x0, int nx, Epi epi,
                           cudaStream_t s) {
-  const stg::Tile T = stg::tile_for(d, 4);
-  stg::sweep_kernel<ORD, SLAB, Epi, 4><<<stg::sweep_grid(d, T, nx), stg::NT, stg::Cfg<4>::kSmemBudget, s>>>(
-      ps, d, disp, T, x0, epi);
+  if (g_gather_mode == 2) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgB>(ps, d, disp, x0, nx, epi, s);
+  else if (g_gather_mode == 3) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgC>(ps, d, disp, x0, nx, epi, s);
+  else launch_staged_cfg<ORD, SLAB, Epi, stg::CfgA>(ps, d, disp, x0, nx, epi, s);
 }
 
 static int advect_impl(const float* src, SlabArgs sg, const int64_t dims[3], const float* disp, const float* factor,
