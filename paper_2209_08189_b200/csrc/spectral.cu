@@ -707,8 +707,9 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   p->smx1 = sizeof(double2) * (d.n1 + 2 * 1 * (size_t)p->Bx1 * (d.n1 + 1));
   const size_t sy = sizeof(double2) * (d.n2 + 2 * (size_t)choose_lines(d.n2, 1, sizeof(double2), 110 * 1024, 16) *
                                                  (d.n2 + 1));
-  if (!p->fast && (p->smz > kSmemBudget || p->smzi > kSmemBudget || sy > kSmemBudget ||
-                   p->smx3 > kSmemBudget || p->smx1 > kSmemBudget)) {
+  // (a 3-component x1 tile over budget only rules out the coupled K on this
+  // plan -- vr_spec_apply / vr_dspec_xpass report VR_ERR_UNSUPPORTED for it)
+  if (!p->fast && (p->smz > kSmemBudget || p->smzi > kSmemBudget || sy > kSmemBudget || p->smx1 > kSmemBudget)) {
     vr_spec_plan_destroy(p);
     return VR_ERR_UNSUPPORTED;
   }
@@ -1102,6 +1103,7 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   if (!p || !in || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && p->fast && xb(p->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048
+  if (kind == VR_SPEC_K && !p->fast && p->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
   if (kind == VR_SPEC_A && d2_ok(p)) return spec_apply_A_d2(p, in, ncomp, alpha, add, out, s);
@@ -1216,7 +1218,10 @@ extern "C" {
 // sendbuf ([q][c][i][jl][kz], complex128 if f64 else complex64).
 int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int nranks, void* sendbuf, void* stream) {
   if (!pl || !in || !sendbuf || nranks < 1 || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
-  if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  if (pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  // the generic mixed-radix path (non-power-of-two sizes, e.g. the CLARITY
+  // shape 2816 x 3016 x 1162) always forward-transforms in f64
+  if (!pl->fast) f64 = 1;
   cudaStream_t s = (cudaStream_t)stream;
   int rc = spec_forward(pl, in, ncomp, s, f64 != 0);
   if (rc) return rc;
@@ -1242,8 +1247,9 @@ int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v
                    void* xout, void* stream) {
   if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3) || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
-  if (!px->fast) return VR_ERR_UNSUPPORTED;
-  if (ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048: 3-component tiles do not fit
+  if (px->fast && ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048: 3-component tiles do not fit
+  if (!px->fast && ncomp == 3 && px->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
+  if (!px->fast) f64 = 1;   // generic path: f64 forward (see vr_dspec_forward)
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
   spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, reinterpret_cast<float2*>(xout));
   VR_CHECK_LAUNCH();
@@ -1254,7 +1260,6 @@ int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v
 int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_global, int l1, double scale,
                         double* out_dev, void* stream) {
   if (!px || !recv || !out_dev || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
-  if (!px->fast) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, j0, n2_global, l1};
   const int nblk = spec_xpass(px, op, true, s, true, recv, nullptr);
@@ -1268,7 +1273,7 @@ int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_globa
 int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add, float* out,
                      void* stream) {
   if (!pl || !recv_inv || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
-  if (!pl->fast || pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  if (pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = pl->nspec * ncomp;
   (void)n;

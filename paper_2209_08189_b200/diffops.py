@@ -106,8 +106,10 @@ class DistSpectralWorkspace:
         self._fin1 = weakref.finalize(self, _destroy_plan, self._pl)
         _lib.check(lib.vr_spec_plan_create(_lib.dims_arg((n1, ctx.L2, n3)), C.byref(self._px)), "vr_spec_plan_create")
         self._fin2 = weakref.finalize(self, _destroy_plan, self._px)
-        if not (lib.vr_spec_plan_is_fast(self._pl) and lib.vr_spec_plan_is_fast(self._px)):
-            raise NotImplementedError("distributed spectral operators need power-of-two N1/P, N2/P, N1, N2, N3/2")
+        # power-of-two sizes run the fast engines (and the fused peer
+        # transposes); any other even size (e.g. the CLARITY shape) the generic
+        # mixed-radix engine, whose forward half is always f64
+        self.generic = not (lib.vr_spec_plan_is_fast(self._pl) and lib.vr_spec_plan_is_fast(self._px))
         nc = 3 * ctx.L1 * n2 * self.n3h          # complex elements per 3-component slab spectrum
         dev = _lib.device()
         self.send = torch.empty(2 * nc, dtype=torch.float64, device=dev)
@@ -119,7 +121,7 @@ class DistSpectralWorkspace:
         # transposes fused into the passes over peer memory (csrc/spectral.cu
         # vr_dspec_*_peer) when the peer mesh is active and the shapes allow
         P = ctx.world
-        self.peer = (ctx.mesh is not None and n2 == 256 and 1 < P <= 8 and (P & (P - 1)) == 0
+        self.peer = (ctx.mesh is not None and not self.generic and n2 == 256 and 1 < P <= 8 and (P & (P - 1)) == 0
                      and os.environ.get("VR_PEER_FUSED", "1") != "0")
         self._dst_cache = {}
 
@@ -201,7 +203,7 @@ class DistSpectralWorkspace:
         ncomp = 3 if x.dim() == 4 else 1
         if out is None:
             out = torch.empty_like(x)
-        f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2)
+        f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2) or self.generic
         P = self.ctx.world
         if self.peer:
             comps = "pipelined" if (ncomp == 3 and kind != _lib.SPEC_K) else "fused"

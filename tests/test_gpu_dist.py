@@ -124,6 +124,10 @@ def case_c2_64(rank, world):
 
 
 def _dist_vs_single(rank, world, n, order):
+    _dist_vs_single_dims(rank, world, (n, n, n), order, 1e-4)
+
+
+def _dist_vs_single_dims(rank, world, dims, order, beta_w):
     """Every operator and a full C2 registration on x1 slabs against the
     single-domain result on the same GPU (identical float32 inputs, made on
     the device): global relative L2 <= 1e-6 per operator (allreduced), PCG
@@ -132,8 +136,9 @@ def _dist_vs_single(rank, world, n, order):
     import paper_2209_08189_b200 as P
     from paper_2209_08189_b200 import dist
     from paper_2209_08189_b200.synth import c2_problem_device
-    g = P.make_grid((n, n, n))
-    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=1e-4, n_t=4, interp_order=order)
+    g = P.make_grid(dims)
+    n = "x".join(map(str, dims))
+    cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=beta_w, n_t=4, interp_order=order)
     m0, m1, l0, l1, vtrue = c2_problem_device(g, order, 4)
     gen = torch.Generator(device="cuda").manual_seed(9)
     w = 0.1 * torch.randn((3,) + g.dims, device="cuda", generator=gen)
@@ -183,12 +188,20 @@ def _dist_vs_single(rank, world, n, order):
               f"{d1.relative_residual:.9e} vs {d0.relative_residual:.9e}; Dice {res.dice.d_a:.9f}", flush=True)
 
 
-def case_parity_256(rank, world):
-    _dist_vs_single(rank, world, 256, "cubic")
-
-
 def case_parity_512(rank, world):
     _dist_vs_single(rank, world, 512, "linear")
+
+
+def case_parity_clarity(rank, world):
+    """C5's CLARITY shape reduced with its prime factors kept: 88 x 104 x 166
+    (2816 = 2^8 11, 3016 = 2^3 13 29, 1162 = 2 7 83 -> 11, 13, 83 here): the
+    generic mixed-radix engine on x1 slabs, linear interpolation and
+    beta_w = 1e-5 as C5 (PAPER.md:691)."""
+    _dist_vs_single_dims(rank, world, (88, 104, 166), "linear", 1e-5)
+
+
+def case_parity_256(rank, world):
+    _dist_vs_single(rank, world, 256, "cubic")
 
 
 @pytest.mark.parametrize("case", ["case_ops_match_single", "case_gn32", "case_c2_64"])
@@ -203,12 +216,12 @@ def test_slab_world2(case):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (gpurun --gpus 2)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity"])
 def test_dist_vs_single_world2(case):
     spawn(case, 2)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs (gpurun --gpus 4)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity"])
 def test_dist_vs_single_world4(case):
     spawn(case, 4)

@@ -243,3 +243,28 @@ def test_1024_spectral_vs_cufft_f64(P, c3):
     assert check(got, lambda c: irfft(rfft(c) - ks[c] * kd)) < TOL
     del kd, got
     torch.cuda.empty_cache()
+
+
+def test_clarity_shape_ops_vs_oracle(P):
+    """C5's CLARITY shape reduced with its odd prime factors kept (88 x 104 x
+    166: 11, 13, 83 -- radix-11/13 butterflies and a direct radix-83 stage in
+    the generic engine): spectral operators, FD8 and a linear SL step against
+    the oracle at 1e-5 (FD8 bit-exact)."""
+    from oracle import velreg_oracle as O
+    dims = (88, 104, 166)
+    g = P.make_grid(dims)
+    rng = np.random.default_rng(21)
+    w = rng.standard_normal((3,) + dims).astype(np.float32)
+    f = rng.random(dims).astype(np.float32)
+    v = (0.2 * O.velocity(2, dims)).astype(np.float32)
+    ops = P.RegOperators.for_grid(g, 1e-2, 1e-5)
+    W = P.VectorField(g, w)
+    w64 = w.astype(np.float64)
+    assert rel_l2(_np(P.apply_A(W, ops).data), O.op_A(w64)) < TOL
+    assert rel_l2(_np(P.apply_inv_shifted_A(W, ops, 1.0).data), O.op_inv_shifted(w64, 1e-2, 1.0)) < TOL
+    assert rel_l2(_np(P.apply_K(W, ops).data), O.op_K(w64, 1e-2, 1e-5)) < TOL
+    np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), O.grad(f))
+    tr = O.Transport(v.astype(np.float64), 4, "linear")
+    tops = P.TransportOperators(P.VectorField(g, v), P.TransportConfig(4, "linear"))
+    got = _np(P.solve_state(P.ScalarField(g, f), tops.v, tops.cfg, tops).values)
+    assert rel_l2(got, tr.state_series(f.astype(np.float64))[-1]) < TOL
