@@ -44,6 +44,7 @@ template <int PPT_, int BUDGET_KB = 36, int CTAS = 6, bool PAD32 = true> struct 
 using CfgA = Cfg<4, 36, 6, true>;
 using CfgB = Cfg<4, 30, 7, false>;
 using CfgC = Cfg<4, 27, 8, false>;
+using CfgD = Cfg<4, 36, 6, false>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

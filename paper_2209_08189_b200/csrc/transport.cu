@@ -486,6 +486,7 @@ static void launch_staged(const PlaneSrc<1, SLAB>& ps, const Dims& d, const floa
                           cudaStream_t s) {
   if (g_gather_mode == 2) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgB>(ps, d, disp, x0, nx, epi, s);
   else if (g_gather_mode == 3) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgC>(ps, d, disp, x0, nx, epi, s);
+  else if (g_gather_mode == 4) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgD>(ps, d, disp, x0, nx, epi, s);
   else launch_staged_cfg<ORD, SLAB, Epi, stg::CfgA>(ps, d, disp, x0, nx, epi, s);
 }
 
