@@ -1011,7 +1011,10 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
 
 // ---- A via the separable line engine (spectral_d2.cuh) ------------------------------
 static int d2_r2(int L) { return L == 256 ? 16 : (L == 128 ? 8 : 0); }
-static int g_d2_threads = 128;   // CTA size of the line passes (128: 3 CTAs / SM at 160 registers)
+// CTA size of the line passes: 128 threads capped at 128 registers -> 4 CTAs / SM
+// (measured at 256^3: 0.703 ms per A; 3 CTAs / SM at 160 registers 0.818 ms;
+// 5 CTAs / SM at 102 registers 0.837 ms; 256-thread CTAs at 2 / SM 0.757 ms)
+static int g_d2_threads = 128;
 
 static bool d2_ok(const vr_spec_plan* p) {
   const Dims& d = p->d;

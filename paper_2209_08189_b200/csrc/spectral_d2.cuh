@@ -75,7 +75,7 @@ __device__ __forceinline__ void line_d2(double2 (&v)[16], float2 (&y)[16], int t
 // x3 lines: one complex line = rows (2p, 2p+1) of the flattened (n1 n2, n3)
 // row array; R2 threads per line, lane = t + R2 q.  acc = D33 v.
 template <int R2, int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) rows_kernel(const float* __restrict__ v, float* __restrict__ acc,
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) rows_kernel(const float* __restrict__ v, float* __restrict__ acc,
                                                       int npairs, int64_t cstride, const double2* __restrict__ tw,
                                                       double scale) {
   constexpr int L = 16 * R2, LPB = NT / R2;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) rows_kernel(const float
 // a contiguous 2 NB-float run.  FINAL = false: acc += D v; FINAL = true:
 // out = alpha (acc + D v) (+ add).  acc may alias out (same element, same thread).
 template <int R2, bool FINAL, int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 1 : 3) strided_kernel(const float* __restrict__ v, float* acc,
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) strided_kernel(const float* __restrict__ v, float* acc,
                                                          const float* __restrict__ add, float* out, int n3, int es,
                                                          int outer_stride, int64_t cstride,
                                                          const double2* __restrict__ tw, double scale, double alpha) {
