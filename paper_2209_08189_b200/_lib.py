@@ -108,7 +108,7 @@ class NativeError(VelregError):
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches accounting)
-LAUNCHES = {"vr_spec_apply_launches": 0, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
+LAUNCHES = {"vr_spec_apply_launches": 0, "vr_trace_rk2": 2, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
             "vr_dspec_forward_peer": 2, "vr_dspec_xpass_peer": 1, "vr_dspec_inverse_peer": 2,
             "vr_spec_plan_is_fast": 0,

@@ -110,6 +110,74 @@ __device__ __forceinline__ void gather_cubic(const Src& src, const Dims& d, int 
   for (int c = 0; c < NC; ++c) out[c] = acc[c];
 }
 
+// 3-component source interleaved as float4 (v1, v2, v3, -): one 16-byte load
+// per tap instead of three scalar loads from three planes (the RK2 trace's
+// velocity gathers).  The arithmetic is gather_cubic / gather_linear's,
+// component by component, so the results are identical.
+struct SrcAoS4 {
+  const float4* __restrict__ q;
+  __device__ __forceinline__ float4 operator()(int idx) const { return __ldg(q + idx); }
+};
+
+template <int ORDER>
+__device__ __forceinline__ void gather_aos3(const SrcAoS4& src, const Dims& d, int ix, int iy, int iz, float tx,
+                                            float ty, float tz, float* out) {
+  if (ORDER == ORDER_LINEAR) {
+    const int i0 = wrap_idx(ix, d.n1), j0 = wrap_idx(iy, d.n2), k0 = wrap_idx(iz, d.n3);
+    const int i1 = next_wrap(i0, d.n1), j1 = next_wrap(j0, d.n2), k1 = next_wrap(k0, d.n3);
+    const int r00 = (i0 * d.n2 + j0) * d.n3, r01 = (i0 * d.n2 + j1) * d.n3;
+    const int r10 = (i1 * d.n2 + j0) * d.n3, r11 = (i1 * d.n2 + j1) * d.n3;
+    const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
+    const float4 a00 = src(r00 + k0), b00 = src(r00 + k1), a01 = src(r01 + k0), b01 = src(r01 + k1);
+    const float4 a10 = src(r10 + k0), b10 = src(r10 + k1), a11 = src(r11 + k0), b11 = src(r11 + k1);
+    const float A00[3] = {a00.x, a00.y, a00.z}, B00[3] = {b00.x, b00.y, b00.z};
+    const float A01[3] = {a01.x, a01.y, a01.z}, B01[3] = {b01.x, b01.y, b01.z};
+    const float A10[3] = {a10.x, a10.y, a10.z}, B10[3] = {b10.x, b10.y, b10.z};
+    const float A11[3] = {a11.x, a11.y, a11.z}, B11[3] = {b11.x, b11.y, b11.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float c00 = A00[c] * sz + B00[c] * tz;
+      const float c01 = A01[c] * sz + B01[c] * tz;
+      const float c10 = A10[c] * sz + B10[c] * tz;
+      const float c11 = A11[c] * sz + B11[c] * tz;
+      const float c0 = c00 * sy + c01 * ty;
+      const float c1 = c10 * sy + c11 * ty;
+      out[c] = c0 * sx + c1 * tx;
+    }
+  } else {
+    float wx[4], wy[4], wz[4];
+    lagrange4(tx, wx);
+    lagrange4(ty, wy);
+    lagrange4(tz, wz);
+    int xo[4], yo[4], zo[4];
+    cubic_idx(wrap_idx(ix, d.n1), d.n1, xo);
+    cubic_idx(wrap_idx(iy, d.n2), d.n2, yo);
+    cubic_idx(wrap_idx(iz, d.n3), d.n3, zo);
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int xa = xo[a] * d.n2;
+      float sa[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int row = (xa + yo[b]) * d.n3;
+        const float4 t0 = src(row + zo[0]), t1 = src(row + zo[1]), t2 = src(row + zo[2]), t3 = src(row + zo[3]);
+        const float T0[3] = {t0.x, t0.y, t0.z}, T1[3] = {t1.x, t1.y, t1.z};
+        const float T2[3] = {t2.x, t2.y, t2.z}, T3[3] = {t3.x, t3.y, t3.z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float sb = wz[0] * T0[c] + wz[1] * T1[c] + wz[2] * T2[c] + wz[3] * T3[c];
+          sa[c] += wy[b] * sb;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += wx[a] * sa[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c] = acc[c];
+  }
+}
+
 template <int ORDER, int NC, class Src>
 __device__ __forceinline__ void gather(const Src& src, const Dims& d, int ix, int iy, int iz, float tx,
                                        float ty, float tz, float* out) {

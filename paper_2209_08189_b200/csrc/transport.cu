@@ -133,6 +133,60 @@ __global__ void __launch_bounds__(256) trace_kernel(const float* __restrict__ v,
   }
 }
 
+// v (3, N) SoA -> (N) float4 AoS (v1, v2, v3, 0) for the trace's velocity gathers
+__global__ void __launch_bounds__(256) soa_to_aos4_kernel(const float* __restrict__ v, int64_t N,
+                                                          float4* __restrict__ q) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) q[i] = make_float4(__ldg(v + i), __ldg(v + N + i), __ldg(v + 2 * N + i), 0.0f);
+}
+
+// trace_kernel's arithmetic with the velocity gathers from the float4 copy
+template <int ORDER, bool FACTORS>
+__global__ void __launch_bounds__(256) trace_aos_kernel(const float* __restrict__ v, const float4* __restrict__ vq,
+                                                        Dims d, float dt, float ih1, float ih2, float ih3,
+                                                        float* __restrict__ disp_f, float* __restrict__ disp_b,
+                                                        const float* __restrict__ div, float* __restrict__ fac_f,
+                                                        float* __restrict__ fac_b) {
+  const int64_t N = d.n();
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N) return;
+  int i, j, k;
+  voxel_ijk(idx, d, i, j, k);
+  const float4 vv = __ldg(vq + idx);
+  const float v1 = vv.x, v2 = vv.y, v3 = vv.z;
+  const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
+  const SrcAoS4 sq{vq};
+  float vs[3];
+  const float half = 0.5f * dt;
+  int ix, iy, iz;
+  float tx, ty, tz;
+  split_coord(i, a1, ix, tx);
+  split_coord(j, a2, iy, ty);
+  split_coord(k, a3, iz, tz);
+  gather_aos3<ORDER>(sq, d, ix, iy, iz, tx, ty, tz, vs);
+  const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
+  disp_f[idx] = f1;
+  disp_f[N + idx] = f2;
+  disp_f[2 * N + idx] = f3;
+  split_coord(i, -a1, ix, tx);
+  split_coord(j, -a2, iy, ty);
+  split_coord(k, -a3, iz, tz);
+  gather_aos3<ORDER>(sq, d, ix, iy, iz, tx, ty, tz, vs);
+  const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
+  disp_b[idx] = b1;
+  disp_b[N + idx] = b2;
+  disp_b[2 * N + idx] = b3;
+  if (FACTORS) {
+    const float* sd[1] = {div};
+    const float denom = 1.0f - half * __ldg(div + idx);
+    float dv;
+    trace_gather<ORDER, false>(sd, d, 0, i, j, k, f1, f2, f3, &dv, 1);
+    fac_f[idx] = (1.0f + half * dv) / denom;
+    trace_gather<ORDER, false>(sd, d, 0, i, j, k, b1, b2, b3, &dv, 1);
+    fac_b[idx] = (1.0f + half * dv) / denom;
+  }
+}
+
 // Periodic single-domain trace on the lean gather (3-D launch, no index
 // divisions, one conditional wrap per axis, immediate-offset x3 taps): the same
 // Heun steps and factors as trace_kernel, 3 components gathered per tap row.
@@ -170,8 +224,10 @@ __global__ void __launch_bounds__(128, 5) trace_lean_kernel(const float* __restr
   }
 }
 
-// 0 (default): general flat-index trace; 1: lean periodic trace -- measured SLOWER on B200
-// (C2 cubic 3.83 vs 2.41 ms per trace), kept behind vr_set_trace_mode for A/B only
+// 0 (default): velocity gathers from a float4 (AoS) copy of v, one 16-B load per
+// tap; 2: general flat-index trace on the SoA field (round-1 default); 1: lean
+// periodic trace -- measured SLOWER on B200 (C2 cubic 3.83 vs 2.41 ms per
+// trace).  Same arithmetic in all three; vr_set_trace_mode selects for A/B.
 static int g_trace_mode = 0;
 
 // ---- one semi-Lagrangian step: dst = interp(src, X) [* factor] --------------
@@ -449,7 +505,19 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
     else if (g_trace_mode == 1)
       trace_lean_kernel<ORD, false><<<vox_grid(d), vox_tpb(d), 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd,
                                                                         disp_bwd, nullptr, nullptr, nullptr);
-    else if (factors)
+    else if (g_trace_mode == 0) {
+      // velocity gathers from a float4 copy (v1, v2, v3, 0): one 16-B load per tap
+      float4* vq = nullptr;
+      if (cudaMallocAsync((void**)&vq, sizeof(float4) * d.n(), s) != cudaSuccess) return VR_ERR_ALLOC;
+      soa_to_aos4_kernel<<<g, 256, 0, s>>>(v, d.n(), vq);
+      if (factors)
+        trace_aos_kernel<ORD, true><<<g, 256, 0, s>>>(v, vq, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
+                                                      fac_jac, fac_adj);
+      else
+        trace_aos_kernel<ORD, false><<<g, 256, 0, s>>>(v, vq, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                       nullptr, nullptr, nullptr);
+      cudaFreeAsync(vq, s);
+    } else if (factors)
       trace_kernel<ORD, true, false><<<g, 256, 0, s>>>(v, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
                                                        fac_jac, fac_adj);
     else

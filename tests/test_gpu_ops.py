@@ -289,8 +289,8 @@ def test_spectral_long_x1_lines(P, dims):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dims", [(32, 32, 32), (16, 20, 24)])
 def test_trace_lean_matches_general(dims):
-    """vr_set_trace_mode A/B: the lean periodic trace (default) against the
-    general flat-index trace, both orders, with and without source factors,
+    """vr_set_trace_mode A/B: the float4-velocity trace (default) against the
+    general flat-index trace and the lean periodic trace, both orders, with source factors,
     including displacements beyond one period (scaled velocity)."""
     import torch
     import paper_2209_08189_b200 as P
@@ -302,7 +302,7 @@ def test_trace_lean_matches_general(dims):
         v = P.VectorField(g, scale * velocity_array(2, g))
         for order in ("cubic", "linear"):
             outs = {}
-            for mode in (0, 1):
+            for mode in (0, 1, 2):
                 prev = lib.vr_set_trace_mode(mode)
                 try:
                     t = P.TransportOperators(v, P.TransportConfig(4, order))
@@ -311,5 +311,6 @@ def test_trace_lean_matches_general(dims):
                 finally:
                     lib.vr_set_trace_mode(prev)
             torch.cuda.synchronize()
-            for x, y in zip(outs[0], outs[1]):
-                assert float((x - y).abs().max()) <= 4e-6 * max(float(x.abs().max()), 1.0), (order, scale)
+            for other in (1, 2):
+                for x, y in zip(outs[0], outs[other]):
+                    assert float((x - y).abs().max()) <= 4e-6 * max(float(x.abs().max()), 1.0), (order, scale, other)
