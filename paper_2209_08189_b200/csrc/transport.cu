@@ -224,8 +224,10 @@ __global__ void __launch_bounds__(128, 5) trace_lean_kernel(const float* __restr
   }
 }
 
-// 0 (default): velocity gathers from a float4 (AoS) copy of v, one 16-B load per
-// tap; 2: general flat-index trace on the SoA field (round-1 default); 1: lean
+// 0 (default): tricubic velocity gathers from a float4 (AoS) copy of v, one 16-B
+// load per tap (C2 trace + FD8 div 2.69 -> 2.38 ms; trilinear unchanged at
+// 0.79 ms, so it keeps the SoA gathers); 2: general flat-index trace on the
+// SoA field (round-1 default); 1: lean
 // periodic trace -- measured SLOWER on B200 (C2 cubic 3.83 vs 2.41 ms per
 // trace).  Same arithmetic in all three; vr_set_trace_mode selects for A/B.
 static int g_trace_mode = 0;
@@ -479,6 +481,22 @@ struct SlabArgs {
   bool on() const { return lo != nullptr; }
 };
 
+// Stream-ordered scratch (cudaMallocAsync) stays in the device's default pool
+// between calls instead of being returned to the OS at every synchronisation
+// (release threshold 0 by default: a 268 MB re-allocation per trace).
+static void keep_pool_memory() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, int w, const float* div, double dt,
                       int order, float* disp_fwd, float* disp_bwd, float* fac_jac, float* fac_adj, void* stream) {
   Dims d;
@@ -505,9 +523,10 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
     else if (g_trace_mode == 1)
       trace_lean_kernel<ORD, false><<<vox_grid(d), vox_tpb(d), 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd,
                                                                         disp_bwd, nullptr, nullptr, nullptr);
-    else if (g_trace_mode == 0) {
+    else if (g_trace_mode == 0 && ORD == ORDER_CUBIC) {   // trilinear: measured equal, keep SoA
       // velocity gathers from a float4 copy (v1, v2, v3, 0): one 16-B load per tap
       float4* vq = nullptr;
+      keep_pool_memory();
       if (cudaMallocAsync((void**)&vq, sizeof(float4) * d.n(), s) != cudaSuccess) return VR_ERR_ALLOC;
       soa_to_aos4_kernel<<<g, 256, 0, s>>>(v, d.n(), vq);
       if (factors)
