@@ -742,6 +742,21 @@ int vr_spec_plan_destroy(vr_spec_plan* p) {
 
 }  // extern "C"
 
+// stream-ordered scratch stays in the default pool between calls (release
+// threshold 0 would hand it back to the OS at every synchronisation)
+static void keep_default_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory once per (device, kernel,
 // size).  Keyed on the kernel's address: template instances that differ only
 // in non-type parameters share a function TYPE, so a per-type static flag
@@ -896,18 +911,6 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   const int nc = op.ncomp;
   const double2* Sd = Sext ? reinterpret_cast<const double2*>(Sext) : p->S;
   float2* Tt = Text ? Text : p->T;
-  if (p->fast && nc == 3 && !reduce && xb(d.n1, 3) == 0) {
-    // x1 lines of 2048: no 3-component tile fits; component-diagonal symbols run
-    // one component at a time (the coupled K symbol is rejected by the callers)
-    SpecOp o1 = op;
-    o1.ncomp = 1;
-    const int64_t cstride = (int64_t)d.n1 * d.n2 * p->n3h;   // single-domain layout [c][i][j][kz]
-    const size_t esz = f64 ? sizeof(double2) : sizeof(float2);
-    int nblk = 0;
-    for (int c = 0; c < 3; ++c)
-      nblk = spec_xpass(p, o1, false, s, f64, reinterpret_cast<const char*>(Sd) + c * cstride * esz, Tt + c * cstride);
-    return nblk;
-  }
   if (p->fast && g_fft_mode && d.n1 == 256 && !reduce && op.kind != VR_SPEC_K && g_xdiag) {
     // component-diagonal symbol: one component per CTA row, no shared tile
     const int nchunks = (p->n3h + 15) / 16;
@@ -949,6 +952,48 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
     if (d.n1 == 1024) XLONG(4, 8, 8)
     XLONG(8, 4, 4)
 #undef XLONG
+  }
+  if (p->fast && g_fft_mode && g_xdiag && !reduce && op.kind == VR_SPEC_K && nc == 3 && !f64 &&
+      (d.n1 == 512 || d.n1 == 1024 || d.n1 == 2048)) {
+    // the coupled K on long x1 lines: forward per component into a scratch
+    // spectrum W (natural frequency order), the 3-component symbol
+    // elementwise, inverse per component (fs::xfwd_long / xsym3 / xinv_long)
+    const int64_t wn = 3 * (int64_t)d.n1 * d.n2 * p->n3h;
+    float2* W = nullptr;
+    keep_default_pool();
+    if (cudaMallocAsync((void**)&W, sizeof(float2) * wn, s) != cudaSuccess) return -1;
+    const float2* S32 = reinterpret_cast<const float2*>(Sd);
+    int nblk = 0;
+#define KLONG(R3, NB)                                                                                        \
+  {                                                                                                          \
+    const int nch = (p->n3h + NB - 1) / NB;                                                                  \
+    const size_t sm = sizeof(float2) * NB * fs::lf3::smem_elems<R3>();                                       \
+    smem_optin(fs::xfwd_long<R3, NB>, sm);                                                                   \
+    smem_optin(fs::xinv_long<R3, NB>, sm);                                                                   \
+    fs::xfwd_long<R3, NB><<<dim3(d.n2 * nch, 3), NB * 16 * R3, sm, s>>>(S32, W, d.n2, p->n3h, p->tw1, op);   \
+    const int64_t per = (int64_t)d.n1 * d.n2 * p->n3h;                                                      \
+    fs::xsym3<<<(unsigned)((per + 255) / 256), 256, 0, s>>>(W, d.n1, d.n2, p->n3h, op);                      \
+    fs::xinv_long<R3, NB><<<dim3(d.n2 * nch, 3), NB * 16 * R3, sm, s>>>(W, Tt, d.n2, p->n3h, p->tw1, op);    \
+    nblk = d.n2 * nch;                                                                                       \
+  }
+    if (d.n1 == 512) KLONG(2, 16)
+    else if (d.n1 == 1024) KLONG(4, 8)
+    else KLONG(8, 4)
+#undef KLONG
+    cudaFreeAsync(W, s);
+    return nblk;
+  }
+  if (p->fast && nc == 3 && !reduce && xb(d.n1, 3) == 0) {
+    // x1 lines of 2048: no 3-component tile fits; component-diagonal symbols run
+    // one component at a time (the coupled K symbol is rejected by the callers)
+    SpecOp o1 = op;
+    o1.ncomp = 1;
+    const int64_t cstride = (int64_t)d.n1 * d.n2 * p->n3h;   // single-domain layout [c][i][j][kz]
+    const size_t esz = f64 ? sizeof(double2) : sizeof(float2);
+    int nblk = 0;
+    for (int c = 0; c < 3; ++c)
+      nblk = spec_xpass(p, o1, false, s, f64, reinterpret_cast<const char*>(Sd) + c * cstride * esz, Tt + c * cstride);
+    return nblk;
   }
   if (p->fast && g_fft_mode && d.n1 == 256 && nc == 3 && !reduce) {
     constexpr int LS = 273;
@@ -1075,6 +1120,9 @@ extern "C" {
 int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp) {
   if (!p) return 0;
   if (kind == VR_SPEC_A && d2_ok(p)) return 3;
+  if (kind == VR_SPEC_K && p->fast && g_fft_mode && g_xdiag &&
+      (p->d.n1 == 512 || p->d.n1 == 1024 || p->d.n1 == 2048))
+    return 7;   // z, y, xfwd_long, xsym3, xinv_long, y', z
   const bool x3split = p->fast && ncomp == 3 && xb(p->d.n1, 3) == 0 && !(g_fft_mode && p->d.n1 == 256);
   const int per = 5 + (x3split ? 2 : 0);
   if (ncomp == 3 && kind != VR_SPEC_K && g_percomp) return 15;
@@ -1105,7 +1153,8 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
                   double shift, double sigma, double alpha, const float* add, float* out, void* stream) {
   if (!p || !in || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
-  if (kind == VR_SPEC_K && p->fast && xb(p->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048
+  if (kind == VR_SPEC_K && p->fast && xb(p->d.n1, 3) == 0 && !(g_fft_mode && g_xdiag && p->d.n1 == 2048))
+    return VR_ERR_UNSUPPORTED;   // N1 > 2048 (2048: the long-line K passes)
   if (kind == VR_SPEC_K && !p->fast && p->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
@@ -1250,7 +1299,8 @@ int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v
                    void* xout, void* stream) {
   if (!px || !recv || !xout || (ncomp != 1 && ncomp != 3) || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
-  if (px->fast && ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;   // N1 >= 2048: 3-component tiles do not fit
+  if (px->fast && ncomp == 3 && xb(px->d.n1, 3) == 0 && !(g_fft_mode && g_xdiag && px->d.n1 == 2048))
+    return VR_ERR_UNSUPPORTED;   // N1 > 2048: 3-component tiles do not fit
   if (!px->fast && ncomp == 3 && px->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
   if (!px->fast) f64 = 1;   // generic path: f64 forward (see vr_dspec_forward)
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
@@ -1337,7 +1387,7 @@ int vr_dspec_xpass_peer(vr_spec_plan* px, int kind, int ncomp, int f64, double b
   if (nranks < 1 || nranks > 8 || me < 0 || me >= nranks || px->d.n1 / l1 != nranks) return VR_ERR_ARG;
   if (kind == VR_SPEC_K && ncomp != 3) return VR_ERR_ARG;
   if (!px->fast) return VR_ERR_UNSUPPORTED;
-  if (ncomp == 3 && xb(px->d.n1, 3) == 0) return VR_ERR_UNSUPPORTED;
+  if (ncomp == 3 && xb(px->d.n1, 3) == 0 && !(g_fft_mode && g_xdiag && px->d.n1 == 2048)) return VR_ERR_UNSUPPORTED;
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
   for (int p = 0; p < nranks; ++p) op.pdst[p] = dst[p];
   op.me = me;

@@ -496,3 +496,79 @@ __global__ void __launch_bounds__(NB * 16 * R3, 1) xdiag_long(const CF* __restri
 
 }  // namespace fs
 }  // namespace vr
+
+namespace vr {
+namespace fs {
+
+// ---- the coupled K symbol on long x1 lines: three passes through a scratch
+// spectrum W ([c][k][j][kz], natural frequency order), since a 3-component
+// register tile of 512-2048-point lines does not fit:
+//   xfwd_long (per component) -> xsym3 (elementwise, couples the components)
+//   -> xinv_long (per component, loads each thread's frequencies, backward stages)
+template <int R3, int NB>
+__global__ void __launch_bounds__(NB * 16 * R3, 1) xfwd_long(const float2* __restrict__ S, float2* __restrict__ W,
+                                                             int n2, int n3h, const double2* __restrict__ twL,
+                                                             SpecOp op) {
+  constexpr int Tn = lf3::T<R3>(), L = 256 * R3, LS = lf3::smem_elems<R3>();
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB, c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
+  const int64_t lstride = (int64_t)n2 * n3h;
+  const float2* sb = S + (int64_t)j * n3h + kz0 + q;
+  float2 v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (ok) v[m] = sb[op.xoff(c, u + Tn * m, lstride)];
+    else v[m] = make_float2(0.f, 0.f);
+  }
+  lf3::forward<float2, R3>(v, u, reinterpret_cast<float2*>(fs_smem) + q * LS, twL);
+  if (ok) {
+    float2* wb = W + ((int64_t)c * L * n2 + j) * n3h + kz0 + q;
+#pragma unroll
+    for (int idx = 0; idx < 16; ++idx) wb[(int64_t)lf3::freq<R3>(u, idx) * lstride] = v[idx];
+  }
+}
+
+// K (apply_symbol, 3 components) at every (k1, j, kz) of W, in place
+__global__ void __launch_bounds__(256) xsym3(float2* __restrict__ W, int L, int n2, int n3h, SpecOp op) {
+  const int64_t per = (int64_t)L * n2 * n3h;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per) return;
+  const int kz = (int)(e % n3h);
+  const int64_t r = e / n3h;
+  const int j = (int)(r % n2), k = (int)(r / n2);
+  double2 vals[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) vals[c] = to_d(W[c * per + e]);
+  apply_symbol(op, (double)signed_freq(k, L), (double)signed_freq(j + op.j0, op.n2g), (double)kz, vals);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) W[c * per + e] = make_float2((float)vals[c].x, (float)vals[c].y);
+}
+
+template <int R3, int NB>
+__global__ void __launch_bounds__(NB * 16 * R3, 1) xinv_long(const float2* __restrict__ W, float2* __restrict__ T,
+                                                             int n2, int n3h, const double2* __restrict__ twL,
+                                                             SpecOp op) {
+  constexpr int Tn = lf3::T<R3>(), L = 256 * R3, LS = lf3::smem_elems<R3>();
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB, c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
+  const int64_t lstride = (int64_t)n2 * n3h;
+  const float2* wb = W + ((int64_t)c * L * n2 + j) * n3h + kz0 + q;
+  float2 v[16];
+#pragma unroll
+  for (int idx = 0; idx < 16; ++idx) v[idx] = ok ? wb[(int64_t)lf3::freq<R3>(u, idx) * lstride] : make_float2(0.f, 0.f);
+  lf3::inverse<float2, R3>(v, u, reinterpret_cast<float2*>(fs_smem) + q * LS, twL);
+  if (ok) {
+    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) *op.out_at(T, c, u + Tn * m, lstride, rowoff) = v[m];
+  }
+}
+
+}  // namespace fs
+}  // namespace vr
