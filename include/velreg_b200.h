@@ -185,6 +185,11 @@ int vr_vecstats(const float* v, int64_t n, double* scratch, double* out4, void* 
 /* ---- vector updates --------------------------------------------------------- */
 int vr_axpby(int64_t n, double a, const float* x, double b, const float* y, float* out, void* stream);
 int vr_pcg_update(int64_t n, double alpha, const float* p, const float* hp, float* x, float* r, void* stream);
+/* PCG step with a device step length: alpha = *rz_dev / *php_dev (f64), then
+ * x_out = x + alpha p, r_out = r - alpha hp (f64 arithmetic, f32 storage);
+ * outputs may alias inputs. */
+int vr_pcg_update2(int64_t n, const double* rz_dev, const double* php_dev, const float* p, const float* hp,
+                   const float* x, const float* r, float* x_out, float* r_out, void* stream);
 int vr_fill(int64_t n, float value, float* out, void* stream);
 
 /* ---- SYN benchmark template (synth.py:77-101 make_template) -------------------

@@ -62,6 +62,7 @@ _SIGS = {
     "vr_vecstats": [_p, _i64, _p, _p, _p],
     "vr_axpby": [_i64, _f64, _p, _f64, _p, _p, _p],
     "vr_pcg_update": [_i64, _f64, _p, _p, _p, _p, _p],
+    "vr_pcg_update2": [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "vr_fill": [_i64, _f32, _p, _p],
     "vr_label_counts": [_p, _p, _i64, _i32, _p, _p],
     "vr_label_range": [_p, _p, _i64, _p, _p],

@@ -186,6 +186,22 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(int64_t n, double alpha
   }
 }
 
+// PCG step with the step length formed on the device, alpha = rz / php (f64,
+// the host's Python division bit for bit), from separate inputs into separate
+// outputs so the caller can still return the previous iterate when php <= 0
+// (optim.py:238-240 negative-curvature exit) after reading both scalars with
+// the next host read.
+__global__ void __launch_bounds__(256) pcg_update2_kernel(int64_t n, const double* __restrict__ rz,
+                                                          const double* __restrict__ php,
+                                                          const float* __restrict__ p, const float* __restrict__ hp,
+                                                          const float* x, const float* r, float* xo, float* ro) {
+  const double alpha = __ldg(rz) / __ldg(php);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    xo[i] = (float)((double)x[i] + alpha * (double)p[i]);
+    ro[i] = (float)((double)r[i] - alpha * (double)hp[i]);
+  }
+}
+
 __global__ void __launch_bounds__(256) fill_kernel(int64_t n, float v, float* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = v;
@@ -329,6 +345,16 @@ int vr_pcg_update(int64_t n, double alpha, const float* p, const float* hp, floa
   if (!p || !hp || !x || !r || n < 0) return VR_ERR_ARG;
   if (n == 0) return VR_OK;
   pcg_update_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(n, alpha, p, hp, x, r);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+int vr_pcg_update2(int64_t n, const double* rz_dev, const double* php_dev, const float* p, const float* hp,
+                   const float* x, const float* r, float* x_out, float* r_out, void* stream) {
+  if (!rz_dev || !php_dev || !p || !hp || !x || !r || !x_out || !r_out || n < 0) return VR_ERR_ARG;
+  if (n == 0) return VR_OK;
+  pcg_update2_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(n, rz_dev, php_dev, p, hp, x, r,
+                                                                                 x_out, r_out);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }

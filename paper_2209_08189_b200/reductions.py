@@ -30,8 +30,9 @@ def _sum(out: torch.Tensor, ctx) -> np.ndarray:
     return res
 
 
-def dots(pairs) -> np.ndarray:
-    """[sum(a*b) for a, b in pairs] (<= 4 pairs, same length) -> float64 array."""
+def dots_dev(pairs) -> torch.Tensor:
+    """[sum(a*b) for a, b in pairs] as a device f64 vector (summed across ranks
+    on the device under a slab decomposition) -- no host read."""
     lib = _lib.lib()
     k = len(pairs)
     assert 1 <= k <= 4
@@ -40,19 +41,46 @@ def dots(pairs) -> np.ndarray:
     a = _lib.ptr_array([p[0] for p in pairs])
     b = _lib.ptr_array([p[1] for p in pairs])
     _lib.check(lib.vr_dots(k, a, b, n, _lib.scratch().data_ptr(), out.data_ptr(), _lib.stream()), "vr_dots")
-    return _sum(out, _ctx(pairs[0][0]))
+    ctx = _ctx(pairs[0][0])
+    if ctx is not None:
+        ctx.allreduce_(out, "sum")
+    return out
+
+
+def host(*devs: torch.Tensor) -> list:
+    """One device->host read for several device result vectors (the solver's
+    sync points), then the deferred non-finite checks; returns numpy arrays."""
+    flat = torch.cat([d.reshape(-1) for d in devs]).cpu().numpy()
+    _lib.run_deferred()
+    res, o = [], 0
+    for d in devs:
+        res.append(flat[o:o + d.numel()])
+        o += d.numel()
+    return res
+
+
+def dots(pairs) -> np.ndarray:
+    """[sum(a*b) for a, b in pairs] (<= 4 pairs, same length) -> float64 array."""
+    return host(dots_dev(pairs))[0]
 
 
 def dot(a: torch.Tensor, b: torch.Tensor) -> float:
     return float(dots([(a, b)])[0])
 
 
-def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> np.ndarray:
+def sqdiff_dev(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> torch.Tensor:
     lib = _lib.lib()
     out = _lib.out_buf(2)
     _lib.check(lib.vr_sqdiff(a.data_ptr(), b.data_ptr(), _lib.ptr(c), _n(a), _lib.scratch().data_ptr(),
                              out.data_ptr(), _lib.stream()), "vr_sqdiff")
-    return _sum(out, _ctx(a))
+    ctx = _ctx(a)
+    if ctx is not None:
+        ctx.allreduce_(out, "sum")
+    return out
+
+
+def sqdiff(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None) -> np.ndarray:
+    return host(sqdiff_dev(a, b, c))[0]
 
 
 def minmax(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
@@ -83,8 +111,8 @@ def minmax_local(a: torch.Tensor, b: torch.Tensor | None = None) -> np.ndarray:
     return out.cpu().numpy()
 
 
-def vecstats(v: torch.Tensor) -> tuple:
-    """(max_x |v(x)|^2, number of non-finite entries, number of non-zero entries)"""
+def vecstats_dev(v: torch.Tensor) -> torch.Tensor:
+    """device f64 [-, max |v|^2, #non-finite, #non-zero] (no host read)"""
     lib = _lib.lib()
     out = _lib.out_buf(4)
     _lib.check(lib.vr_vecstats(v.data_ptr(), _n(v) // 3, _lib.scratch().data_ptr(), out.data_ptr(),
@@ -93,7 +121,12 @@ def vecstats(v: torch.Tensor) -> tuple:
     if ctx is not None:
         ctx.allreduce_(out[1:2], "max")
         ctx.allreduce_(out[2:4], "sum")
-    o = out.cpu().numpy()
+    return out
+
+
+def vecstats(v: torch.Tensor) -> tuple:
+    """(max_x |v(x)|^2, number of non-finite entries, number of non-zero entries)"""
+    o = vecstats_dev(v).cpu().numpy()
     return float(o[1]), int(o[2]), int(o[3])
 
 
@@ -105,6 +138,14 @@ def axpby(a: float, x: torch.Tensor, b: float = 0.0, y: torch.Tensor | None = No
     _lib.check(_lib.lib().vr_axpby(_n(x), float(a), x.data_ptr(), float(b), _lib.ptr(y), out.data_ptr(),
                                    _lib.stream()), "vr_axpby")
     return out
+
+
+def pcg_update2(rz_dev: torch.Tensor, php_dev: torch.Tensor, p: torch.Tensor, hp: torch.Tensor, x: torch.Tensor,
+                r: torch.Tensor, x_out: torch.Tensor, r_out: torch.Tensor) -> None:
+    """x_out = x + alpha p, r_out = r - alpha hp with alpha = rz / php formed on the device."""
+    _lib.check(_lib.lib().vr_pcg_update2(_n(x), rz_dev.data_ptr(), php_dev.data_ptr(), p.data_ptr(), hp.data_ptr(),
+                                         x.data_ptr(), r.data_ptr(), x_out.data_ptr(), r_out.data_ptr(),
+                                         _lib.stream()), "vr_pcg_update2")
 
 
 def pcg_update(alpha: float, p: torch.Tensor, hp: torch.Tensor, x: torch.Tensor, r: torch.Tensor) -> None:

@@ -128,12 +128,18 @@ class TransportOperators:
     divergence kernel.  The factors are stored as ratios
     jac_factor = jac_numer / jac_denom and adj_factor = adj_numer / adj_denom."""
 
-    def __init__(self, v: VectorField, cfg: TransportConfig):
-        _check_finite_velocity(v)
+    def __init__(self, v: VectorField, cfg: TransportConfig, defer_checks: bool = False):
         self.v = v
         self.cfg = cfg
         self.grid = v.grid
         self.ctx = _dist.for_grid(v.grid.dims)
+        if defer_checks and self.ctx is None:
+            # read with the caller's next reduction (ObjectiveState): same error
+            from .reductions import vecstats_dev
+            st = vecstats_dev(v.data)
+            _lib.defer_check(st[2:3], TransportError("velocity field contains non-finite values"))
+        else:
+            _check_finite_velocity(v)
         if self.ctx is None:
             self.div = fd8_divergence_t(v.data)
             disp_f, disp_b, self.jac_factor, self.adj_factor = _trace(v.data, v.grid.dims, cfg.dt, cfg.interp_order,
@@ -143,8 +149,9 @@ class TransportOperators:
         self.forward = Characteristics(v.grid, disp_f, cfg.dt)
         self.backward = Characteristics(v.grid, disp_b, cfg.dt)
         # non-finite flags: [0] eager checks, [1] / [2] the matvec's deferred
-        # incremental-state / adjoint checks
-        self.flags = torch.zeros((3, 1), dtype=torch.int32, device=v.data.device)
+        # incremental-state / adjoint checks, [3] / [4] ObjectiveState's deferred
+        # state / adjoint checks
+        self.flags = torch.zeros((5, 1), dtype=torch.int32, device=v.data.device)
 
     # ---- x1-slab decomposition (dist.py) ----------------------------------------
     def _trace_slab(self, v: torch.Tensor):
@@ -275,7 +282,7 @@ def _ops_for(v: VectorField, cfg: TransportConfig, ops) -> TransportOperators:
 
 
 def solve_state_series(m0: ScalarField, v: VectorField, cfg: TransportConfig,
-                       ops: TransportOperators = None) -> torch.Tensor:
+                       ops: TransportOperators = None, _deferred: bool = False) -> torch.Tensor:
     """All n_t + 1 snapshots of the transported template, shape (n_t+1,) + dims
     (transport.py:124-135)."""
     if m0.grid != v.grid:
@@ -283,10 +290,11 @@ def solve_state_series(m0: ScalarField, v: VectorField, cfg: TransportConfig,
     ops = _ops_for(v, cfg, ops)
     series = torch.empty((cfg.n_t + 1,) + tuple(m0.values.shape), dtype=torch.float32, device=m0.values.device)
     series[0].copy_(m0.values)
-    flag = ops.arm()
+    slot = 3 if _deferred else 0
+    flag = ops.arm(slot)
     for j in range(cfg.n_t):
         ops.advect_step(series[j], out=series[j + 1], flag=flag if j == cfg.n_t - 1 else None)
-    ops.raise_if_flagged("state solve")
+    ops.raise_if_flagged("state solve", slot, _deferred)
     return series
 
 
@@ -323,8 +331,9 @@ def solve_adjoint(final_lambda: ScalarField, v: VectorField, cfg: TransportConfi
 
 
 def _adjoint_sweep(series: torch.Tensor, ops: TransportOperators, cfg: TransportConfig,
-                   deferred: bool = False) -> None:
-    slot = 2 if deferred else 0
+                   deferred: bool = False, slot: int | None = None) -> None:
+    if slot is None:
+        slot = 2 if deferred else 0
     flag = ops.arm(slot)
     for j in range(cfg.n_t - 1, -1, -1):
         ops.sweep(series[j + 1], ops.backward.displacement, factor=ops.adj_factor, out=series[j],
