@@ -141,18 +141,20 @@ __global__ void __launch_bounds__(256) soa_to_aos4_kernel(const float* __restric
 }
 
 // trace_kernel's arithmetic with the velocity gathers from the float4 copy
-template <int ORDER, bool FACTORS>
-__global__ void __launch_bounds__(256) trace_aos_kernel(const float* __restrict__ v, const float4* __restrict__ vq,
-                                                        Dims d, float dt, float ih1, float ih2, float ih3,
-                                                        float* __restrict__ disp_f, float* __restrict__ disp_b,
-                                                        const float* __restrict__ div, float* __restrict__ fac_f,
-                                                        float* __restrict__ fac_b) {
+// (SLAB: vq is the ghost-extended slab, L1 + 2w planes, x1 clamped as in trace_gather)
+template <int ORDER, bool FACTORS, bool SLAB>
+__global__ void __launch_bounds__(256) trace_aos_kernel(const float4* __restrict__ vq, Dims d, int w, float dt,
+                                                        float ih1, float ih2, float ih3, float* __restrict__ disp_f,
+                                                        float* __restrict__ disp_b, const float* __restrict__ div,
+                                                        float* __restrict__ fac_f, float* __restrict__ fac_b) {
   const int64_t N = d.n();
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= N) return;
   int i, j, k;
   voxel_ijk(idx, d, i, j, k);
-  const float4 vv = __ldg(vq + idx);
+  const Dims ds{SLAB ? d.n1 + 2 * w : d.n1, d.n2, d.n3};   // source dims
+  const int sidx = SLAB ? idx + w * d.n2 * d.n3 : idx;    // own voxel in the source
+  const float4 vv = __ldg(vq + sidx);
   const float v1 = vv.x, v2 = vv.y, v3 = vv.z;
   const float a1 = dt * v1 * ih1, a2 = dt * v2 * ih2, a3 = dt * v3 * ih3;
   const SrcAoS4 sq{vq};
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(256) trace_aos_kernel(const float* __restrict_
   split_coord(i, a1, ix, tx);
   split_coord(j, a2, iy, ty);
   split_coord(k, a3, iz, tz);
-  gather_aos3<ORDER>(sq, d, ix, iy, iz, tx, ty, tz, vs);
+  if (SLAB) ix = clampi(ix + w, 1, ds.n1 - 3);
+  gather_aos3<ORDER>(sq, ds, ix, iy, iz, tx, ty, tz, vs);
   const float f1 = half * (v1 + vs[0]) * ih1, f2 = half * (v2 + vs[1]) * ih2, f3 = half * (v3 + vs[2]) * ih3;
   disp_f[idx] = f1;
   disp_f[N + idx] = f2;
@@ -171,18 +174,19 @@ __global__ void __launch_bounds__(256) trace_aos_kernel(const float* __restrict_
   split_coord(i, -a1, ix, tx);
   split_coord(j, -a2, iy, ty);
   split_coord(k, -a3, iz, tz);
-  gather_aos3<ORDER>(sq, d, ix, iy, iz, tx, ty, tz, vs);
+  if (SLAB) ix = clampi(ix + w, 1, ds.n1 - 3);
+  gather_aos3<ORDER>(sq, ds, ix, iy, iz, tx, ty, tz, vs);
   const float b1 = -half * (v1 + vs[0]) * ih1, b2 = -half * (v2 + vs[1]) * ih2, b3 = -half * (v3 + vs[2]) * ih3;
   disp_b[idx] = b1;
   disp_b[N + idx] = b2;
   disp_b[2 * N + idx] = b3;
   if (FACTORS) {
     const float* sd[1] = {div};
-    const float denom = 1.0f - half * __ldg(div + idx);
+    const float denom = 1.0f - half * __ldg(div + sidx);
     float dv;
-    trace_gather<ORDER, false>(sd, d, 0, i, j, k, f1, f2, f3, &dv, 1);
+    trace_gather<ORDER, SLAB>(sd, ds, w, i, j, k, f1, f2, f3, &dv, 1);
     fac_f[idx] = (1.0f + half * dv) / denom;
-    trace_gather<ORDER, false>(sd, d, 0, i, j, k, b1, b2, b3, &dv, 1);
+    trace_gather<ORDER, SLAB>(sd, ds, w, i, j, k, b1, b2, b3, &dv, 1);
     fac_b[idx] = (1.0f + half * dv) / denom;
   }
 }
@@ -511,7 +515,30 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
   const float ih1 = (float)(n1_global / kTwoPi), ih2 = (float)(d.n2 / kTwoPi), ih3 = (float)(d.n3 / kTwoPi);
   const unsigned g = grid_for(d.n(), 256);
   VR_DISPATCH_ORDER(order, {
-    if (slab && factors)
+    if (g_trace_mode == 0 && ORD == ORDER_CUBIC) {
+      // tricubic velocity gathers from a float4 copy (v1, v2, v3, 0) of v (or
+      // of the ghost-extended slab): one 16-B load per tap (trilinear measured
+      // equal and keeps the SoA gathers)
+      const int64_t Ne = slab ? (int64_t)(d.n1 + 2 * w) * d.n2 * d.n3 : d.n();
+      float4* vq = nullptr;
+      keep_pool_memory();
+      if (cudaMallocAsync((void**)&vq, sizeof(float4) * Ne, s) != cudaSuccess) return VR_ERR_ALLOC;
+      soa_to_aos4_kernel<<<grid_for(Ne, 256), 256, 0, s>>>(v, Ne, vq);
+      const int ww = slab ? w : 0;
+      if (slab && factors)
+        trace_aos_kernel<ORD, true, true><<<g, 256, 0, s>>>(vq, d, ww, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                            div, fac_jac, fac_adj);
+      else if (slab)
+        trace_aos_kernel<ORD, false, true><<<g, 256, 0, s>>>(vq, d, ww, (float)dt, ih1, ih2, ih3, disp_fwd,
+                                                             disp_bwd, nullptr, nullptr, nullptr);
+      else if (factors)
+        trace_aos_kernel<ORD, true, false><<<g, 256, 0, s>>>(vq, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
+                                                             div, fac_jac, fac_adj);
+      else
+        trace_aos_kernel<ORD, false, false><<<g, 256, 0, s>>>(vq, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd,
+                                                              disp_bwd, nullptr, nullptr, nullptr);
+      cudaFreeAsync(vq, s);
+    } else if (slab && factors)
       trace_kernel<ORD, true, true><<<g, 256, 0, s>>>(v, d, w, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
                                                       fac_jac, fac_adj);
     else if (slab)
@@ -523,20 +550,7 @@ static int trace_impl(const float* v, const int64_t dims[3], int64_t n1_global, 
     else if (g_trace_mode == 1)
       trace_lean_kernel<ORD, false><<<vox_grid(d), vox_tpb(d), 0, s>>>(v, d, (float)dt, ih1, ih2, ih3, disp_fwd,
                                                                         disp_bwd, nullptr, nullptr, nullptr);
-    else if (g_trace_mode == 0 && ORD == ORDER_CUBIC) {   // trilinear: measured equal, keep SoA
-      // velocity gathers from a float4 copy (v1, v2, v3, 0): one 16-B load per tap
-      float4* vq = nullptr;
-      keep_pool_memory();
-      if (cudaMallocAsync((void**)&vq, sizeof(float4) * d.n(), s) != cudaSuccess) return VR_ERR_ALLOC;
-      soa_to_aos4_kernel<<<g, 256, 0, s>>>(v, d.n(), vq);
-      if (factors)
-        trace_aos_kernel<ORD, true><<<g, 256, 0, s>>>(v, vq, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
-                                                      fac_jac, fac_adj);
-      else
-        trace_aos_kernel<ORD, false><<<g, 256, 0, s>>>(v, vq, d, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd,
-                                                       nullptr, nullptr, nullptr);
-      cudaFreeAsync(vq, s);
-    } else if (factors)
+    else if (factors)
       trace_kernel<ORD, true, false><<<g, 256, 0, s>>>(v, d, 0, (float)dt, ih1, ih2, ih3, disp_fwd, disp_bwd, div,
                                                        fac_jac, fac_adj);
     else
