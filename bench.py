@@ -372,9 +372,25 @@ def run_ours(args):
         with open(tfile) as fh:
             traffic = json.load(fh).get(dominant)
     step_ms = t_step * 1e3
-    kernels = {k: {"avg_ms": round(v[0], 5), "launches_per_step": v[1] // max(args.steps, 1),
-                   "share_of_step": round(v[0] * v[1] / max(args.steps, 1) / step_ms, 4)}
-               for k, v in kern.items() if v[1] > 0}
+    # algorithmic HBM bytes per voxel / point of each timed entry:
+    # sweeps 20 B/point (+4 factor), incremental step 44 B, FD8 16 B, spectral
+    # vector operator 24 B, RK2 trace 48 B (v + div in, 2 displacements + 2
+    # factors out), body force 92 B (5 lambda + 5 grad-m snapshots in, 3 out)
+    algo = {"vr_advect": 20.0, "vr_advect_slab": 20.0, "vr_incstate_step": 44.0, "vr_incstate_step_slab": 44.0,
+            "vr_fd8_grad": 16.0, "vr_fd8_grad_slab": 16.0, "vr_spec_apply": 24.0, "vr_trace_rk2": 48.0,
+            "vr_trace_rk2_slab": 48.0, "vr_body_force": 92.0}
+    vox_local = g.num_voxels // ws
+    kernels = {}
+    for k, v in kern.items():
+        if v[1] <= 0:
+            continue
+        e = {"avg_ms": round(v[0], 5), "launches_per_step": v[1] // max(args.steps, 1),
+             "share_of_step": round(v[0] * v[1] / max(args.steps, 1) / step_ms, 4)}
+        if k in algo and v[0] > 0:
+            gbs = algo[k] * vox_local / (v[0] * 1e-3) / 1e9
+            e["algorithmic_gbs"] = round(gbs, 1)
+            e["hbm_frac"] = round(gbs / peaks["hbm_gbs"], 4)
+        kernels[k] = e
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -87,6 +87,9 @@ struct IC {
 // along x1.  CTA = TXB x TYB threads = a TY x TZ (x2, x3) tile.
 constexpr int TXB = 16, TYB = 16, RY = 2, TZ = 2 * TXB, TY = RY * TYB, HALO = 4, NTHR = TXB * TYB;
 constexpr int NS = 4;  // cp.async ring depth (plane steps in flight)
+#ifndef VR_FD8_CTAS
+#define VR_FD8_CTAS 3      // resident CTAs / SM the tile kernel is compiled for
+#endif
 
 // One plane step in shared memory.  MODE 0 (gradient): a (TY+8) x (TZ+8) tile
 // of f.  MODE 1 (divergence): a (TY+8) x TZ tile of v2 (x2 halo only) and a
@@ -127,7 +130,7 @@ __device__ __forceinline__ float2 lds2(const float* p) { return *reinterpret_cas
 // read the 4 ghost planes before (lo) / after (hi) it.  The x2/x3 tiles only
 // ever read local planes.  Requires N3 even (the reference grid's dims are).
 template <int MODE, bool SLAB>
-__global__ void __launch_bounds__(NTHR, 2) fd8_kernel(const float* __restrict__ f, const float* __restrict__ lo,
+__global__ void __launch_bounds__(NTHR, VR_FD8_CTAS) fd8_kernel(const float* __restrict__ f, const float* __restrict__ lo,
                                                       const float* __restrict__ hi, Dims d, float h1, float h2,
                                                       float h3, float r1, float r2, float r3, unsigned dlo,
                                                       unsigned dspan,

@@ -20,16 +20,6 @@ def _ctx(t: torch.Tensor):
     return _dist.for_shape(t.shape)
 
 
-def _sum(out: torch.Tensor, ctx) -> np.ndarray:
-    """Host copy of a device result vector, summed across ranks (on device) when
-    the operands are slabs of an active decomposition."""
-    if ctx is not None:
-        ctx.allreduce_(out, "sum")
-    res = out.cpu().numpy()
-    _lib.run_deferred()
-    return res
-
-
 def dots_dev(pairs) -> torch.Tensor:
     """[sum(a*b) for a, b in pairs] as a device f64 vector (summed across ranks
     on the device under a slab decomposition) -- no host read."""
