@@ -824,9 +824,42 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
 }
 
 // forward Z + Y passes into p->S (as double2, or as float2 when !f64 on the fast path)
+// x3 passes of 256-point rows as paired-row four-step kernels (fs::zfwd256_pair /
+// zinv256_pair); vr_set_spectral_tuning(2, 0) selects the Stockham kernels
+static int g_zpair = 1;
+static bool zpair_ok(const vr_spec_plan* p) {
+  return g_zpair && g_fft_mode && p->fast && p->d.n3 == 256 && (p->d.n1 * p->d.n2) % 2 == 0;
+}
+template <typename CF>
+static void zfwd_pair(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s) {
+  const int npairs = p->d.n1 * p->d.n2 / 2;
+  const size_t sm = sizeof(CF) * 16 * fs::line_smem<16>();
+  smem_optin(fs::zfwd256_pair<CF>, sm);
+  fs::zfwd256_pair<CF><<<dim3((npairs + 15) / 16, ncomp), 256, sm, s>>>(in, npairs, p->d.n(), p->nspec, p->tw3,
+                                                                        reinterpret_cast<CF*>(p->S));
+}
+static void zinv_pair(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
+  const int npairs = p->d.n1 * p->d.n2 / 2;
+  const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
+  smem_optin(fs::zinv256_pair, sm);
+  fs::zinv256_pair<<<dim3((npairs + 15) / 16, ncomp), 256, sm, s>>>(p->T, npairs, p->d.n(), p->nspec, p->tw3, out,
+                                                                    add);
+}
+
 static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s, bool f64 = true) {
   const Dims& d = p->d;
   const int nrows = d.n1 * d.n2;
+  if (p->fast && zpair_ok(p)) {
+    if (f64) {
+      zfwd_pair<double2>(p, in, ncomp, s);
+      launch_axis<double2>(p, p->S, 2, ncomp, 0, s);
+    } else {
+      zfwd_pair<float2>(p, in, ncomp, s);
+      launch_axis<float2>(p, reinterpret_cast<float2*>(p->S), 2, ncomp, 0, s);
+    }
+    VR_CHECK_LAUNCH();
+    return VR_OK;
+  }
   if (p->fast) {
     const int M = d.n3 / 2;
 #define L_Z(MM)                                                                                            \
@@ -858,6 +891,11 @@ static int spec_forward(vr_spec_plan* p, const float* in, int ncomp, cudaStream_
 
 // Z forward pass only (fast path) into p->S
 static void spec_forward_z(vr_spec_plan* p, const float* in, int ncomp, cudaStream_t s, bool f64) {
+  if (zpair_ok(p)) {
+    if (f64) zfwd_pair<double2>(p, in, ncomp, s);
+    else zfwd_pair<float2>(p, in, ncomp, s);
+    return;
+  }
   const Dims& d = p->d;
   const int nrows = d.n1 * d.n2;
   const int M = d.n3 / 2;
@@ -877,6 +915,10 @@ static void spec_forward_z(vr_spec_plan* p, const float* in, int ncomp, cudaStre
 
 // Z inverse pass only (fast path): p->T -> out (+ add)
 static void spec_inverse_z(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
+  if (zpair_ok(p)) {
+    zinv_pair(p, ncomp, add, out, s);
+    return;
+  }
   const Dims& d = p->d;
   const int nrows = d.n1 * d.n2;
   const int M = d.n3 / 2;
@@ -890,6 +932,10 @@ static void spec_inverse_z(vr_spec_plan* p, int ncomp, const float* add, float* 
 static void spec_inverse_yz(vr_spec_plan* p, int ncomp, const float* add, float* out, cudaStream_t s) {
   const Dims& d = p->d;
   launch_axis<float2>(p, p->T, 2, ncomp, 1, s);
+  if (zpair_ok(p)) {
+    zinv_pair(p, ncomp, add, out, s);
+    return;
+  }
   const int nrows = d.n1 * d.n2;
   if (p->fast) {
     const int M = d.n3 / 2;
@@ -1131,6 +1177,12 @@ int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp) {
 
 int vr_set_spectral_tuning(int key, int value) {
   // key 1: per-component scheduling of diagonal symbols (1 = on, 0 = all components per pass)
+  // key 2: paired-row four-step x3 passes for 256-point rows (1 = on, 0 = Stockham)
+  if (key == 2) {
+    const int prev = g_zpair;
+    g_zpair = value;
+    return prev;
+  }
   if (key == 1) {
     const int prev = g_percomp;
     g_percomp = value;

@@ -572,3 +572,102 @@ __global__ void __launch_bounds__(NB * 16 * R3, 1) xinv_long(const float2* __res
 
 }  // namespace fs
 }  // namespace vr
+
+namespace vr {
+namespace fs {
+
+// ---- x3 passes for 256-point real rows: two rows as one complex line --------
+// Forward: z = a + i b (rows 2p, 2p+1), four-step line FFT, then the two half
+// spectra from Z and its mirror (A_k = (Z_k + conj Z_{N-k}) / 2,
+// B_k = (Z_k - conj Z_{N-k}) / 2i); the mirror Z_{N-k} of thread t's Z_{t+16u}
+// lives in thread (16 - t) & 15 at u' = 15 - u (thread 0: its own (16 - u) & 15),
+// fetched with one shuffle per value.  Inverse: Z_k = A_k + i B_k with the
+// Hermitian mirror for k > 128 (DC / Nyquist imaginary parts dropped, as
+// pocketfft's c2r does), inverse line FFT, a = Re, b = Im (+ addend).
+// 16 threads per pair, 16 pairs per 256-thread CTA, grid (pairs / 16, ncomp).
+template <typename CF>
+__global__ void __launch_bounds__(256, sizeof(CF) == 8 ? 3 : 2) zfwd256_pair(const float* __restrict__ in, int npairs,
+                                                                          int64_t nvox, int64_t nspec,
+                                                                          const double2* __restrict__ tw,
+                                                                          CF* __restrict__ S) {
+  constexpr int L = 256, NH = 129;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int t = threadIdx.x & 15, q = threadIdx.x >> 4;
+  const int pr = blockIdx.x * 16 + q;
+  const bool ok = pr < npairs;
+  const float* ra = in + blockIdx.y * nvox + (int64_t)(ok ? pr : 0) * 2 * L;
+  const float* rb = ra + L;
+  CF v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    v[m].x = __ldg(ra + t + 16 * m);
+    v[m].y = __ldg(rb + t + 16 * m);
+  }
+  line_fft<CF, 16>(v, t, reinterpret_cast<CF*>(fs_smem) + q * line_smem<16>(), tw, false);
+  // thread t holds Z[t + 16 u] in v[u]
+  using R = decltype(v[0].x);
+  const int lane = threadIdx.x & 31, base = lane & 16;
+  const int partner = base + ((16 - t) & 15);
+  CF* da = S + blockIdx.y * nspec + (int64_t)(ok ? pr : 0) * 2 * NH;
+  CF* db = da + NH;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    CF m;
+    m.x = __shfl_sync(0xffffffffu, v[15 - u].x, partner);
+    m.y = __shfl_sync(0xffffffffu, v[15 - u].y, partner);
+    if (t == 0) m = v[(16 - u) & 15];
+    const int k = t + 16 * u;
+    if (ok && k <= 128) {
+      CF A, B;
+      A.x = R(0.5) * (v[u].x + m.x);
+      A.y = R(0.5) * (v[u].y - m.y);
+      B.x = R(0.5) * (v[u].y + m.y);
+      B.y = R(-0.5) * (v[u].x - m.x);
+      da[k] = A;
+      db[k] = B;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) zinv256_pair(const float2* __restrict__ T, int npairs, int64_t nvox,
+                                                      int64_t nspec, const double2* __restrict__ tw,
+                                                      float* __restrict__ out, const float* __restrict__ add) {
+  constexpr int L = 256, NH = 129;
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  const int t = threadIdx.x & 15, q = threadIdx.x >> 4;
+  const int pr = blockIdx.x * 16 + q;
+  const bool ok = pr < npairs;
+  const float2* sa = T + blockIdx.y * nspec + (int64_t)(ok ? pr : 0) * 2 * NH;
+  const float2* sb = sa + NH;
+  float2 v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int k = t + 16 * m;
+    const bool mir = k > 128;
+    const int kk = mir ? L - k : k;
+    float2 A = __ldg(sa + kk), B = __ldg(sb + kk);
+    if (kk == 0 || kk == 128) { A.y = 0.f; B.y = 0.f; }   // c2r ignores Im of DC / Nyquist
+    if (mir) { A.y = -A.y; B.y = -B.y; }
+    v[m] = make_float2(A.x - B.y, A.y + B.x);               // Z = A + i B
+  }
+  line_fft<float2, 16>(v, t, reinterpret_cast<float2*>(fs_smem) + q * line_smem<16>(), tw, true);
+  if (ok) {
+    float* oa = out + blockIdx.y * nvox + (int64_t)pr * 2 * L;
+    float* ob = oa + L;
+    const float* aa = add ? add + blockIdx.y * nvox + (int64_t)pr * 2 * L : nullptr;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int x = t + 16 * u;
+      float ya = v[u].x, yb = v[u].y;
+      if (aa) {
+        ya += __ldg(aa + x);
+        yb += __ldg(aa + L + x);
+      }
+      oa[x] = ya;
+      ob[x] = yb;
+    }
+  }
+}
+
+}  // namespace fs
+}  // namespace vr
