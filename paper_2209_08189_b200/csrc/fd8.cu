@@ -88,7 +88,7 @@ struct IC {
 constexpr int TXB = 16, TYB = 16, RY = 2, TZ = 2 * TXB, TY = RY * TYB, HALO = 4, NTHR = TXB * TYB;
 constexpr int NS = 4;  // cp.async ring depth (plane steps in flight)
 #ifndef VR_FD8_CTAS
-#define VR_FD8_CTAS 3      // resident CTAs / SM the tile kernel is compiled for
+#define VR_FD8_CTAS 2      // resident CTAs / SM (3, at 80 registers: divergence 0.100 vs 0.085 ms)
 #endif
 
 // One plane step in shared memory.  MODE 0 (gradient): a (TY+8) x (TZ+8) tile
