@@ -22,9 +22,6 @@ namespace vr {
 __constant__ float kFd8[4] = {(float)(4.0 / 5.0), (float)(-1.0 / 5.0), (float)(4.0 / 105.0),
                               (float)(-1.0 / 280.0)};
 
-// Quotients outside that range (tiny or huge sums) take an f64 division rounded
-// once to f32, which is the correctly rounded f32 quotient: 53 >= 2 * 24 + 2
-// bits make the double rounding innocuous (subnormal results included).
 // x / h correctly rounded from the precomputed r = RN(1/h) (Markstein):
 // q = RN(x r) is within 1 ulp of x/h, e = x - q h is exact by FMA, and
 // RN(q + e r) = RN(x/h) -- the same bits as IEEE division, in 3 instructions.
@@ -54,6 +51,31 @@ __device__ __forceinline__ float fd8_sum(float p0, float p1, float p2, float p3,
   out = __fadd_rn(out, __fmul_rn(kFd8[2], __fsub_rn(p2, m2)));
   out = __fadd_rn(out, __fmul_rn(kFd8[3], __fsub_rn(p3, m3)));
   return out;
+}
+
+// The 12 sums of one micro-tile step (x1 / x2 / x3 derivative, 4 voxels each)
+// divided by h: IEEE division where the reciprocal form is not proven exact.
+struct F12 {
+  float v[12];
+};
+__device__ __noinline__ F12 fd8_div_ieee(F12 s, float h1, float h2, float h3, float r1, float r2, float r3,
+                                         unsigned dlo, unsigned dspan) {
+  // Tiny sums with a normal quotient (2^-125 <= |x/h|, |x| < 2^-100) are
+  // scaled by 2^64 into the verified range first: both scalings are exact.
+  const bool verified = dlo == 0x0d800000u;
+  F12 o;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const float h = i < 4 ? h1 : (i < 8 ? h2 : h3), r = i < 4 ? r1 : (i < 8 ? r2 : r3);
+    const float x = s.v[i], ax = fabsf(x);
+    if (!div_needs_ieee(x, dlo, dspan))
+      o.v[i] = div_fast(x, h, r);
+    else if (verified && ax < 0x1p-100f && ax >= 0x1p-125f * h)
+      o.v[i] = __fmul_rn(div_fast(__fmul_rn(x, 0x1p64f), h, r), 0x1p-64f);
+    else
+      o.v[i] = __fdiv_rn(x, h);
+  }
+  return o;
 }
 
 template <int V>
@@ -294,18 +316,24 @@ __global__ void __launch_bounds__(NTHR, VR_FD8_CTAS) fd8_kernel(const float* __r
         for (int c = 0; c < 2; ++c)
           ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
                   div_needs_ieee(g3[r][c], dlo, dspan);
-      if (ieee) {
-        // rare (tiny / huge sums): f64 division rounded once to f32 -- the
-        // correctly rounded f32 quotient (53 >= 2 * 24 + 2 bits, so the double
-        // rounding is innocuous, subnormal results included); inline, no
-        // out-of-line call spilling the micro-tile through local memory
+      if (ieee) {  // rare: out of line, so the 9 unrolled steps stay compact
+        F12 sv;
 #pragma unroll
         for (int r = 0; r < RY; ++r)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            g1[r][c] = (float)((double)g1[r][c] / (double)h1);
-            g2[r][c] = (float)((double)g2[r][c] / (double)h2);
-            g3[r][c] = (float)((double)g3[r][c] / (double)h3);
+            sv.v[r * 2 + c] = g1[r][c];
+            sv.v[4 + r * 2 + c] = g2[r][c];
+            sv.v[8 + r * 2 + c] = g3[r][c];
+          }
+        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            g1[r][c] = sv.v[r * 2 + c];
+            g2[r][c] = sv.v[4 + r * 2 + c];
+            g3[r][c] = sv.v[8 + r * 2 + c];
           }
       } else {
 #pragma unroll
@@ -540,15 +568,24 @@ __global__ void __launch_bounds__(256, 2) fd8_rows_kernel(const float* __restric
       for (int c = 0; c < 4; ++c)
         ieee |= div_needs_ieee(g1[r][c], dlo, dspan) | div_needs_ieee(g2[r][c], dlo, dspan) |
                 div_needs_ieee(g3[r][c], dlo, dspan);
-    if (ieee) {   // f64 division rounded once: the correctly rounded quotient (see fd8_kernel)
+    if (ieee) {
 #pragma unroll
-      for (int r = 0; r < RY; ++r)
+      for (int r = 0; r < RY; ++r) {
+        F12 sv;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          g1[r][c] = (float)((double)g1[r][c] / (double)h1);
-          g2[r][c] = (float)((double)g2[r][c] / (double)h2);
-          g3[r][c] = (float)((double)g3[r][c] / (double)h3);
+          sv.v[c] = g1[r][c];
+          sv.v[4 + c] = g2[r][c];
+          sv.v[8 + c] = g3[r][c];
         }
+        sv = fd8_div_ieee(sv, h1, h2, h3, r1, r2, r3, dlo, dspan);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g1[r][c] = sv.v[c];
+          g2[r][c] = sv.v[4 + c];
+          g3[r][c] = sv.v[8 + c];
+        }
+      }
     } else {
 #pragma unroll
       for (int r = 0; r < RY; ++r)
@@ -614,8 +651,10 @@ void fd8_rows_run(cudaStream_t s, const float* in, const float* lo, const float*
 // kernel gradient 0.092 ms / divergence 0.145 ms vs tile kernel 0.084 / 0.085 ms
 // (one barrier + mbarrier wait per plane for all 8 warps, and the 8-plane
 // window preload per 16-plane chunk), so the tile kernel stays the default.
-// (A per-element inline IEEE-division select was also measured: 0.094 ms --
-// the one-branch-per-micro-tile form below is faster on the common path.)
+// (A per-element inline IEEE-division select was also measured: 0.094 ms, and
+// an inline f64 division for flagged micro-tiles 0.146 vs 0.120 ms on the C2
+// state series -- the out-of-line one-branch-per-micro-tile form below is
+// faster on the common path.)
 static int g_fd8_mode = 0;
 
 template <int MODE, bool SLAB>
