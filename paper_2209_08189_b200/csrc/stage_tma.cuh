@@ -283,3 +283,219 @@ inline dim3 sweep_grid(const Dims& d, const Tile& T, int nplanes) {
 
 }  // namespace stg
 }  // namespace vr
+
+namespace vr {
+namespace stg {
+
+// ---- warp-tiled, double-buffered staged sweep ---------------------------------
+// Each WARP owns a stream of tiles (32 consecutive x3 voxels x WR x2 rows of
+// one x1 plane) and keeps the NEXT tile's source box in flight while it
+// gathers the current one: per warp two box buffers and two mbarriers, box
+// bounds from warp reductions, one cp.async.bulk per box row issued by the
+// warp's own lanes -- no CTA-wide barrier anywhere, so a warp never waits for
+// another warp's copy.  (The CTA-tiled kernel above spends ~1/3 of its stall
+// samples in the mbarrier wait for its single box.)  Taps and arithmetic are
+// the CTA kernel's, so results equal the direct gather's to the ulp.
+constexpr int WR = 2;          // x2 rows per warp tile (points per lane)
+constexpr int WCAP = 2048;     // floats per box buffer (8 KB)
+constexpr int WWARPS = 4;      // warps per CTA
+
+struct WBox {
+  int x0, y0, s, nx, ny, len, pitch, ok;
+};
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int ORDER, bool SLAB, class Epi>
+__global__ void __launch_bounds__(WWARPS * 32, 3) wsweep_kernel(PlaneSrc<1, SLAB> src, Dims d,
+                                                               const float* __restrict__ disp, int x0, int nx,
+                                                               Epi epi) {
+  constexpr int LO = ORDER == ORDER_CUBIC ? 1 : 0;
+  constexpr int HI = ORDER == ORDER_CUBIC ? 2 : 1;
+  extern __shared__ __align__(128) float wbox[];
+  __shared__ __align__(8) unsigned long long bars[WWARPS][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf0 = wbox + (size_t)(w * 2) * WCAP;
+  float* buf1 = buf0 + WCAP;
+  const unsigned bar0 = smem_u32(&bars[w][0]), bar1 = smem_u32(&bars[w][1]);
+  if (lane == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar1, 1);
+  }
+  __syncwarp();
+  const int64_t N = d.n();
+  const int psz = d.n2 * d.n3;
+  const int tk = d.n3 >> 5, tj = d.n2 / WR;
+  const int64_t ntiles = (int64_t)nx * tj * tk;
+  const int64_t stride = (int64_t)gridDim.x * WWARPS;
+  int64_t t = (int64_t)blockIdx.x * WWARPS + w;
+
+  // per-tile lane state
+  auto tile_pos = [&](int64_t tt, int& i, int& j0, int& k) {
+    const int kb = (int)(tt % tk);
+    const int64_t r = tt / tk;
+    const int jb = (int)(r % tj);
+    i = (int)(r / tj) + x0;
+    j0 = jb * WR;
+    k = kb * 32 + lane;
+  };
+  auto load_disp = [&](int64_t tt, float (&dv)[3][WR]) {
+    int i, j0, k;
+    tile_pos(tt, i, j0, k);
+#pragma unroll
+    for (int p = 0; p < WR; ++p) {
+      const int id = (i * d.n2 + j0 + p) * d.n3 + k;
+      dv[0][p] = __ldg(disp + id);
+      dv[1][p] = __ldg(disp + N + id);
+      dv[2][p] = __ldg(disp + 2 * N + id);
+    }
+  };
+  // box of a tile (uniform across the warp) and the copies into `buf` on `bar`
+  auto make_box = [&](int64_t tt, const float (&dv)[3][WR]) -> WBox {
+    int i, j0, k;
+    tile_pos(tt, i, j0, k);
+    int mn1 = INT_MAX, mx1 = INT_MIN, mn2 = INT_MAX, mx2 = INT_MIN, mn3 = INT_MAX, mx3 = INT_MIN;
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < WR; ++p) {
+      const PointSplit<ORDER, SLAB> ps(src, d, i, j0 + p, k, dv[0][p], dv[1][p], dv[2][p]);
+      bad |= ps.bad;
+      mn1 = min(mn1, ps.b1); mx1 = max(mx1, ps.b1);
+      mn2 = min(mn2, ps.b2); mx2 = max(mx2, ps.b2);
+      mn3 = min(mn3, ps.b3); mx3 = max(mx3, ps.b3);
+    }
+    WBox b;
+    mn1 = __reduce_min_sync(~0u, mn1); mx1 = __reduce_max_sync(~0u, mx1);
+    mn2 = __reduce_min_sync(~0u, mn2); mx2 = __reduce_max_sync(~0u, mx2);
+    mn3 = __reduce_min_sync(~0u, mn3); mx3 = __reduce_max_sync(~0u, mx3);
+    const bool anybad = __any_sync(~0u, bad);
+    b.x0 = mn1 - LO;
+    b.nx = mx1 - mn1 + LO + HI + 1;
+    b.y0 = mn2 - LO;
+    b.ny = mx2 - mn2 + LO + HI + 1;
+    b.s = floor4(mn3 - LO);
+    b.len = ((mx3 + HI + 1 - b.s) + 3) & ~3;
+    b.pitch = (b.len & 31) == 0 ? b.len + 4 : b.len;
+    b.ok = !anybad && b.len <= d.n3 && b.ny <= d.n2 && (SLAB || b.nx <= d.n1) && b.nx * b.ny <= 64 &&
+           b.nx * b.ny * b.pitch <= WCAP;
+    return b;
+  };
+  auto issue = [&](const WBox& b, float* buf, unsigned bar) {
+    if (!b.ok) return;
+    __syncwarp();
+    fence_proxy_async();   // the warp's earlier generic reads of `buf` before the async-proxy writes
+    if (lane == 0) mbar_expect_tx(bar, (unsigned)(b.nx * b.ny * b.len * 4));
+    __syncwarp();
+    int s = b.s % d.n3;
+    if (s < 0) s += d.n3;
+    const int first = min(b.len, d.n3 - s);
+    const int nrows = b.nx * b.ny;
+    for (int r = lane; r < nrows; r += 32) {
+      const int xr = r / b.ny, yr = r - xr * b.ny;
+      int x = b.x0 + xr;
+      if (!SLAB) x = wrap1(x, d.n1);
+      int y = (b.y0 + yr) % d.n2;
+      if (y < 0) y += d.n2;
+      const float* row = src.plane(0, x, psz) + y * d.n3;
+      const unsigned dst = smem_u32(buf + r * b.pitch);
+      bulk_g2s(dst, row + s, (unsigned)first * 4u, bar);
+      if (first < b.len) bulk_g2s(dst + first * 4u, row, (unsigned)(b.len - first) * 4u, bar);
+    }
+  };
+
+  float dv[3][WR];
+  WBox box;
+  unsigned ph0 = 0, ph1 = 0;
+  if (t < ntiles) {
+    load_disp(t, dv);
+    box = make_box(t, dv);
+    issue(box, buf0, bar0);
+  }
+  for (int it = 0; t < ntiles; ++it, t += stride) {
+    const bool odd = it & 1;
+    float* cur = odd ? buf1 : buf0;
+    float* nxt = odd ? buf0 : buf1;
+    const unsigned cbar = odd ? bar1 : bar0, nbar = odd ? bar0 : bar1;
+    // prefetch the next tile's displacements and box
+    const int64_t t2 = t + stride;
+    float dv2[3][WR];
+    WBox box2;
+    box2.ok = 0;
+    if (t2 < ntiles) {
+      load_disp(t2, dv2);
+      box2 = make_box(t2, dv2);
+      issue(box2, nxt, nbar);
+    }
+    int i, j0, k;
+    tile_pos(t, i, j0, k);
+    if (box.ok) {
+      mbar_wait(cbar, odd ? ph1 : ph0);
+      if (odd) ph1 ^= 1u; else ph0 ^= 1u;
+#pragma unroll
+      for (int p = 0; p < WR; ++p) {
+        const int j = j0 + p;
+        const PointSplit<ORDER, SLAB> ps(src, d, i, j, k, dv[0][p], dv[1][p], dv[2][p]);
+        float o;
+        if (ORDER == ORDER_CUBIC) {
+          float wx[4], wy[4], wz[4];
+          lagrange4(ps.t1, wx);
+          lagrange4(ps.t2, wy);
+          lagrange4(ps.t3, wz);
+          const int xs = box.ny * box.pitch;
+          const float* base = cur + ((ps.b1 - 1 - box.x0) * box.ny + (ps.b2 - 1 - box.y0)) * box.pitch +
+                              (ps.b3 - 1 - box.s);
+          float acc = 0.0f;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            float sa = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float* r = base + a * xs + c * box.pitch;
+              const float sb = wz[0] * r[0] + wz[1] * r[1] + wz[2] * r[2] + wz[3] * r[3];
+              sa += wy[c] * sb;
+            }
+            acc += wx[a] * sa;
+          }
+          o = acc;
+        } else {
+          const float* r0 = cur + ((ps.b1 - box.x0) * box.ny + (ps.b2 - box.y0)) * box.pitch + (ps.b3 - box.s);
+          const float* r1 = r0 + box.pitch;
+          const float* r2 = r0 + box.ny * box.pitch;
+          const float* r3 = r2 + box.pitch;
+          const float tz = ps.t3, ty = ps.t2, tx = ps.t1;
+          const float sz = 1.0f - tz, sy = 1.0f - ty, sx = 1.0f - tx;
+          const float c00 = r0[0] * sz + r0[1] * tz;
+          const float c01 = r1[0] * sz + r1[1] * tz;
+          const float c10 = r2[0] * sz + r2[1] * tz;
+          const float c11 = r3[0] * sz + r3[1] * tz;
+          const float c0 = c00 * sy + c01 * ty;
+          const float c1 = c10 * sy + c11 * ty;
+          o = c0 * sx + c1 * tx;
+        }
+        epi((i * d.n2 + j) * d.n3 + k, o);
+      }
+    } else {   // box over budget / non-finite displacement: direct gather (same taps and order)
+#pragma unroll 1
+      for (int p = 0; p < WR; ++p) {
+        const int j = j0 + p;
+        float o;
+        gather_disp_lean<ORDER, 1, SLAB>(src, d, i, j, k, dv[0][p], dv[1][p], dv[2][p], &o);
+        epi((i * d.n2 + j) * d.n3 + k, o);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < WR; ++p) {
+      dv[0][p] = dv2[0][p];
+      dv[1][p] = dv2[1][p];
+      dv[2][p] = dv2[2][p];
+    }
+    box = box2;
+  }
+}
+
+inline bool wsweep_ok(const Dims& d) { return d.n3 % 32 == 0 && d.n2 % WR == 0; }
+
+}  // namespace stg
+}  // namespace vr

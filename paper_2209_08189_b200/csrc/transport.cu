@@ -7,6 +7,7 @@
 // absolute radians wrapped to [0,2pi) (transport.py:75); both describe the same
 // point, the displacement keeps full fp32 precision for the interpolation
 // fraction at any grid size.
+#include <algorithm>
 #include "common.cuh"
 #include "interp.cuh"
 #include "stage_tma.cuh"
@@ -583,8 +584,31 @@ static void launch_staged_cfg(const PlaneSrc<1, SLAB>& ps, const Dims& d, const 
 }
 
 template <int ORD, bool SLAB, class Epi>
+static void launch_wsweep(const PlaneSrc<1, SLAB>& ps, const Dims& d, const float* disp, int x0, int nx, Epi epi,
+                          cudaStream_t s) {
+  const size_t sm = sizeof(float) * stg::WCAP * 2 * stg::WWARPS;
+  static int slots = 0;
+  if (!slots) {
+    cudaFuncSetAttribute(stg::wsweep_kernel<ORD, SLAB, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stg::wsweep_kernel<ORD, SLAB, Epi>, stg::WWARPS * 32, sm);
+    slots = sms * (per > 0 ? per : 1);
+  }
+  const int64_t ntiles = (int64_t)nx * (d.n2 / stg::WR) * (d.n3 / 32);
+  const int64_t need = (ntiles + stg::WWARPS - 1) / stg::WWARPS;
+  const unsigned grid = (unsigned)std::min<int64_t>(need, slots);
+  stg::wsweep_kernel<ORD, SLAB, Epi><<<grid, stg::WWARPS * 32, sm, s>>>(ps, d, disp, x0, nx, epi);
+}
+
+template <int ORD, bool SLAB, class Epi>
 static void launch_staged(const PlaneSrc<1, SLAB>& ps, const Dims& d, const float* disp, int x0, int nx, Epi epi,
                           cudaStream_t s) {
+  if (g_gather_mode == 5 && stg::wsweep_ok(d)) {
+    launch_wsweep<ORD, SLAB, Epi>(ps, d, disp, x0, nx, epi, s);
+    return;
+  }
   if (g_gather_mode == 2) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgB>(ps, d, disp, x0, nx, epi, s);
   else if (g_gather_mode == 3) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgC>(ps, d, disp, x0, nx, epi, s);
   else if (g_gather_mode == 4) launch_staged_cfg<ORD, SLAB, Epi, stg::CfgD>(ps, d, disp, x0, nx, epi, s);

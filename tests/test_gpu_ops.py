@@ -245,7 +245,7 @@ def test_staged_gather_matches_direct(P, dims, scale):
         tops = P.TransportOperators(v, P.TransportConfig(4, order))
         for disp in (tops.forward.displacement, tops.backward.displacement, rnd):
             outs = {}
-            for mode in (0, 1):
+            for mode in (0, 1, 5):
                 prev = lib.vr_set_gather_mode(mode)
                 try:
                     res = [transport.advect(f, disp, order, factor=tops.adj_factor), transport.advect(f, disp, order)]
@@ -260,7 +260,7 @@ def test_staged_gather_matches_direct(P, dims, scale):
                 finally:
                     lib.vr_set_gather_mode(prev)
             torch.cuda.synchronize()
-            for mode in (1,):
+            for mode in (1, 5):
                 for x, y in zip(outs[0], outs[mode]):
                     # same taps and arithmetic order; FMA contraction may differ by an ulp
                     assert float((x - y).abs().max()) <= 4e-6 * float(x.abs().max()), (order, dims, mode)
