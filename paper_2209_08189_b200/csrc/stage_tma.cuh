@@ -296,6 +296,10 @@ namespace stg {
 // another warp's copy.  (The CTA-tiled kernel above spends ~1/3 of its stall
 // samples in the mbarrier wait for its single box.)  Taps and arithmetic are
 // the CTA kernel's, so results equal the direct gather's to the ulp.
+// MEASURED SLOWER on B200 (C2 advect 0.550 vs 0.293 ms, incremental step 0.617
+// vs 0.342): a 32-voxel-wide box row is a ~160-B bulk copy, 3.5x more copy
+// requests per byte than the CTA tile's ~560-B rows, and 8 KB double buffers
+// leave 12 warps / SM.  Kept behind vr_set_gather_mode(5) as the record.
 constexpr int WR = 2;          // x2 rows per warp tile (points per lane)
 constexpr int WCAP = 2048;     // floats per box buffer (8 KB)
 constexpr int WWARPS = 4;      // warps per CTA
