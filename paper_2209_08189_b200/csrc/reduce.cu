@@ -73,6 +73,31 @@ __global__ void __launch_bounds__(kRedThreads) dot_partials_kernel(DotArgs args,
   block_reduce_store<K>(acc, partials + (int64_t)blockIdx.x * K, VR_RED_SUM);
 }
 
+// The same sums with every distinct operand array loaded once per element:
+// PCG's (r.z, z.z) and the norms (g.g) name an array twice, and a load per
+// operand re-reads it (a dot is HBM-bound).  Same products, same order: the
+// results equal dot_partials_kernel's bit for bit.
+struct DotArgsU {
+  const float* src[8];
+  int ia[4], ib[4];
+};
+
+template <int K, int NS>
+__global__ void __launch_bounds__(kRedThreads) dotu_partials_kernel(DotArgsU args, int64_t n,
+                                                                    double* __restrict__ partials) {
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) v[u] = (double)__ldg(args.src[u] + i);
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] += v[args.ia[q]] * v[args.ib[q]];
+  }
+  block_reduce_store<K>(acc, partials + (int64_t)blockIdx.x * K, VR_RED_SUM);
+}
+
 // sum (a-b)^2 and sum (c-b)^2 in one pass (relative residual numerator/denominator)
 __global__ void __launch_bounds__(kRedThreads) sqdiff_partials_kernel(const float* __restrict__ a,
                                                                       const float* __restrict__ b,
@@ -289,6 +314,29 @@ int vr_dots(int k, const float* const* a, const float* const* b, int64_t n, doub
   }
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned nb = red_blocks(n);
+  // distinct operand arrays
+  DotArgsU u{};
+  int ns = 0;
+  auto slot = [&](const float* ptr) {
+    for (int t = 0; t < ns; ++t)
+      if (u.src[t] == ptr) return t;
+    u.src[ns] = ptr;
+    return ns++;
+  };
+  for (int q = 0; q < k; ++q) {
+    u.ia[q] = slot(a[q]);
+    u.ib[q] = slot(b[q]);
+  }
+  if (ns < 2 * k && ns <= 3 && k <= 2) {   // an array is named twice: load it once
+#define VR_DOTU(KK, NN) dotu_partials_kernel<KK, NN><<<nb, kRedThreads, 0, s>>>(u, n, scratch)
+    if (k == 1) VR_DOTU(1, 1);
+    else if (ns == 2) VR_DOTU(2, 2);
+    else VR_DOTU(2, 3);
+#undef VR_DOTU
+    fold_partials_kernel<<<1, 256, 0, s>>>(scratch, nb, k, k, VR_RED_SUM, out);
+    VR_CHECK_LAUNCH();
+    return VR_OK;
+  }
   switch (k) {
     case 1: dot_partials_kernel<1><<<nb, kRedThreads, 0, s>>>(args, n, scratch); break;
     case 2: dot_partials_kernel<2><<<nb, kRedThreads, 0, s>>>(args, n, scratch); break;
