@@ -687,8 +687,10 @@ int vr_spec_plan_create(const int64_t dims[3], vr_spec_plan** out) {
   if (!rc && p->fast) rc = upload_stage_twiddles(d.n1, &p->stw1);
   if (!rc && p->fast) rc = upload_stage_twiddles(d.n2, &p->stw2);
   if (!rc && p->fast) rc = upload_stage_twiddles(d.n3 / 2, &p->stw3h);
-  if (!rc && cudaMalloc(&p->S, sizeof(double2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
-  if (!rc && cudaMalloc(&p->T, sizeof(float2) * 3 * p->nspec) != cudaSuccess) rc = VR_ERR_ALLOC;
+  // S / T (the 3-component spectrum scratch, 36 B per voxel) are allocated on
+  // first use (ensure_scratch): the transposed-block plan of the peer path
+  // never touches them -- its input is the receive buffer and its output goes
+  // straight to the peers
   const int maxblk = d.n2 * p->n3h + 1024;
   if (!rc && cudaMalloc(&p->partials, sizeof(double) * maxblk) != cudaSuccess) rc = VR_ERR_ALLOC;
   if (rc) {
@@ -821,6 +823,12 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
   axis_kernel<C><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, L, es, n_outer, outer_stride, p->nspec,
                                                                  p->n3h, ax2 ? p->rp2 : p->rp1,
                                                                  ax2 ? p->tw2 : p->tw1, B, inv);
+}
+
+static int ensure_scratch(vr_spec_plan* p, bool need_s = true, bool need_t = true) {
+  if (need_s && !p->S && cudaMalloc(&p->S, sizeof(double2) * 3 * p->nspec) != cudaSuccess) return VR_ERR_ALLOC;
+  if (need_t && !p->T && cudaMalloc(&p->T, sizeof(float2) * 3 * p->nspec) != cudaSuccess) return VR_ERR_ALLOC;
+  return VR_OK;
 }
 
 // forward Z + Y passes into p->S (as double2, or as float2 when !f64 on the fast path)
@@ -1210,7 +1218,9 @@ int vr_spec_apply(vr_spec_plan* p, int kind, const float* in, int ncomp, double 
   if (kind == VR_SPEC_K && !p->fast && p->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
-  if (kind == VR_SPEC_A && d2_ok(p)) return spec_apply_A_d2(p, in, ncomp, alpha, add, out, s);
+  const bool sep = kind == VR_SPEC_A && d2_ok(p);
+  if (int rc = ensure_scratch(p, !sep, true)) return rc;
+  if (sep) return spec_apply_A_d2(p, in, ncomp, alpha, add, out, s);
   const bool f64 = needs_f64(kind);
   if (ncomp == 3 && kind != VR_SPEC_K && g_percomp) {
     // component-diagonal symbol: run the five passes one component at a time
@@ -1244,7 +1254,9 @@ int vr_prolong_spectral(vr_spec_plan* pc, vr_spec_plan* pf, const float* in, int
   if (pf->d.n1 < pc->d.n1 || pf->d.n2 < pc->d.n2 || pf->d.n3 < pc->d.n3) return VR_ERR_DIMS;
   if (pc->d.n1 % 2 || pc->d.n2 % 2 || pc->d.n3 % 2) return VR_ERR_DIMS;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = spec_forward(pc, in, ncomp, s);
+  int rc = ensure_scratch(pc);
+  if (!rc) rc = ensure_scratch(pf);
+  if (!rc) rc = spec_forward(pc, in, ncomp, s);
   if (rc) return rc;
   launch_axis<double2>(pc, pc->S, 1, ncomp, 0, s);
   const int64_t n = pf->nspec * ncomp;
@@ -1261,7 +1273,8 @@ int vr_h1_energy(vr_spec_plan* p, const float* f, double* out_dev, void* stream)
   if (!p || !f || !out_dev) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const Dims& d = p->d;
-  int rc = spec_forward(p, f, 1, s);
+  int rc = ensure_scratch(p);
+  if (!rc) rc = spec_forward(p, f, 1, s);
   if (rc) return rc;
   SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, 0, d.n2, d.n1};
   const int nblk = spec_xpass(p, op, true, s);
@@ -1327,7 +1340,8 @@ int vr_dspec_forward(vr_spec_plan* pl, const float* in, int ncomp, int f64, int 
   // shape 2816 x 3016 x 1162) always forward-transforms in f64
   if (!pl->fast) f64 = 1;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = spec_forward(pl, in, ncomp, s, f64 != 0);
+  int rc = ensure_scratch(pl);
+  if (!rc) rc = spec_forward(pl, in, ncomp, s, f64 != 0);
   if (rc) return rc;
   const int64_t n = pl->nspec * ncomp;
   const unsigned g = (unsigned)((ncomp * pl->d.n1 * pl->d.n2 + 7) / 8);
@@ -1355,6 +1369,8 @@ int vr_dspec_xpass(vr_spec_plan* px, int kind, int ncomp, int f64, double beta_v
     return VR_ERR_UNSUPPORTED;   // N1 > 2048: 3-component tiles do not fit
   if (!px->fast && ncomp == 3 && px->smx3 > kSmemBudget) return VR_ERR_UNSUPPORTED;
   if (!px->fast) f64 = 1;   // generic path: f64 forward (see vr_dspec_forward)
+  if (!px->fast)
+    if (int rc = ensure_scratch(px)) return rc;
   SpecOp op{kind, ncomp, beta_v, beta_w, shift, alpha / (double)n_global, sigma, j0, n2_global, l1};
   spec_xpass(px, op, false, (cudaStream_t)stream, f64 != 0, recv, reinterpret_cast<float2*>(xout));
   VR_CHECK_LAUNCH();
@@ -1366,6 +1382,8 @@ int vr_dspec_h1_partial(vr_spec_plan* px, const void* recv, int j0, int n2_globa
                         double* out_dev, void* stream) {
   if (!px || !recv || !out_dev || l1 < 1 || px->d.n1 % l1) return VR_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!px->fast)
+    if (int rc = ensure_scratch(px)) return rc;
   SpecOp op{VR_SPEC_IDENTITY, 1, 0, 0, 0, 1.0, 0, j0, n2_global, l1};
   const int nblk = spec_xpass(px, op, true, s, true, recv, nullptr);
   finalize_sum_kernel<<<1, 1024, 0, s>>>(px->partials, nblk, scale, out_dev);
@@ -1379,6 +1397,7 @@ int vr_dspec_inverse(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nran
                      void* stream) {
   if (!pl || !recv_inv || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (pl->d.n2 % nranks) return VR_ERR_UNSUPPORTED;
+  if (int rc = ensure_scratch(pl)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = pl->nspec * ncomp;
   (void)n;
@@ -1407,6 +1426,7 @@ int vr_dspec_forward_peer(vr_spec_plan* pl, const float* in, int ncomp, int f64,
                           void* const* dst, void* stream) {
   if (!in || !dst || (ncomp != 1 && ncomp != 3) || me < 0 || me >= nranks) return VR_ERR_ARG;
   if (!peer_ok(pl, nranks)) return VR_ERR_UNSUPPORTED;
+  if (int rc = ensure_scratch(pl)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   spec_forward_z(pl, in, ncomp, s, f64 != 0);
   fs::X2Peer pe{};
@@ -1453,6 +1473,7 @@ int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int
                           float* out, void* stream) {
   if (!recv_inv || !out || (ncomp != 1 && ncomp != 3)) return VR_ERR_ARG;
   if (!peer_ok(pl, nranks)) return VR_ERR_UNSUPPORTED;
+  if (int rc = ensure_scratch(pl)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   fs::X2Peer pe{};
   pe.l2shift = log2i(nranks);

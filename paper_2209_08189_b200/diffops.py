@@ -111,10 +111,9 @@ class DistSpectralWorkspace:
         # mixed-radix engine, whose forward half is always f64
         self.generic = not (lib.vr_spec_plan_is_fast(self._pl) and lib.vr_spec_plan_is_fast(self._px))
         nc = 3 * ctx.L1 * n2 * self.n3h          # complex elements per 3-component slab spectrum
-        dev = _lib.device()
-        self.send = torch.empty(2 * nc, dtype=torch.float64, device=dev)
+        self._nc = nc
+        self._send = self._xout = None   # staging of the packed (non-fused) path, allocated on first use
         self.recv = ctx.buffer(f"spec_recv_{n1}x{n2}x{n3}", torch.float64, 2 * nc)     # peers write here
-        self.xout = torch.empty(2 * nc, dtype=torch.float32, device=dev)
         self.irecv = ctx.buffer(f"spec_irecv_{n1}x{n2}x{n3}", torch.float32, 2 * nc)
         self.per_comp = ctx.L1 * n2 * self.n3h   # complex elements per component
         self.device = torch.cuda.current_device()
@@ -124,6 +123,18 @@ class DistSpectralWorkspace:
         self.peer = (ctx.mesh is not None and not self.generic and n2 == 256 and 1 < P <= 8 and (P & (P - 1)) == 0
                      and os.environ.get("VR_PEER_FUSED", "1") != "0")
         self._dst_cache = {}
+
+    @property
+    def send(self) -> torch.Tensor:
+        if self._send is None:
+            self._send = torch.empty(2 * self._nc, dtype=torch.float64, device=_lib.device())
+        return self._send
+
+    @property
+    def xout(self) -> torch.Tensor:
+        if self._xout is None:
+            self._xout = torch.empty(2 * self._nc, dtype=torch.float32, device=_lib.device())
+        return self._xout
 
     # ---- peer (fused-transpose) path ---------------------------------------------
     def _dst(self, view: torch.Tensor):

@@ -1,7 +1,7 @@
 """Measured HBM footprint per voxel of one registration.
 
-    python tools/memory_plan.py [--n 256] [--nt 4] [--layout auto|stored|lean] [--order cubic]
-    torchrun --nproc-per-node 2 ... tools/memory_plan.py --n 512      # x1 slabs
+    python tools/memory_plan.py [--size 256] [--nt 4] [--layout auto|stored|lean] [--order cubic]
+    torchrun --nproc-per-node 2 ... tools/memory_plan.py --size 512      # x1 slabs
 
 Runs C2's sphere problem (synth.c2_problem_device) through `register` and
 reports, per rank, the torch allocator's peak (fields, PCG vectors, series)
@@ -33,7 +33,7 @@ TARGETS = {"C3": ((1024, 1024, 1024), 4), "C5": ((2816, 3016, 1162), 8)}
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--size", type=int, default=256)
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--order", default="cubic")
     ap.add_argument("--layout", default="auto")
@@ -49,7 +49,7 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=dev)
     runtime.set_grad_layout(a.layout)
     from paper_2209_08189_b200 import dist as pdist
-    g = P.make_grid((a.n,) * 3)
+    g = P.make_grid((a.size,) * 3)
     act = pdist.activate(pdist.SlabContext(g.dims) if world > 1 else None)
     act.__enter__()
     m0, m1, l0, l1, vtrue = c2_problem_device(g, "linear", 16)
@@ -63,10 +63,10 @@ def main():
     peak = torch.cuda.max_memory_allocated(dev) - base_alloc
     free1, _ = torch.cuda.mem_get_info(dev)
     outside = (total - free1) - used0 - torch.cuda.memory_reserved(dev)
-    nloc = m0.data.numel()
+    nloc = m0.values.numel()
     bpv_torch = peak / nloc
     bpv_lib = max(outside, 0) / nloc
-    line = {"rank": rank, "world": world, "n": a.n, "n_t": a.nt, "order": a.order, "layout": a.layout,
+    line = {"rank": rank, "world": world, "n": a.size, "n_t": a.nt, "order": a.order, "layout": a.layout,
             "local_voxels": nloc, "matvecs": res.diagnostics.matvecs,
             "torch_peak_gb": peak / 2 ** 30, "outside_torch_gb": outside / 2 ** 30,
             "bytes_per_voxel_torch": round(bpv_torch, 1), "bytes_per_voxel_outside": round(bpv_lib, 1),
