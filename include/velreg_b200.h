@@ -276,6 +276,29 @@ int vr_dspec_xpass_peer(vr_spec_plan* px, int kind, int ncomp, int f64, double b
 int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int nranks, const float* add,
                           float* out, void* stream);
 
+/* A = -Laplacian on x1 slabs through the separable line engine (replaces the
+ * 3-D path above for A; reference diffops.py:116-118, optim.py:109-116).
+ * pl = slab plan {L1, N2, N3}, px = block plan {N1, N2 / nranks, N3};
+ * N3 and N2 in {128, 256}, N1 in {128 .. 2048} (powers of two), N2 / nranks
+ * even.  Sequence per operator (one stream; the caller signals / waits the
+ * epoch flags between the phases):
+ *   vr_dspec_a_rows     acc = D33 in, and every slab row stored into the block
+ *                       buffer blk[j / L2] ([c][N1][L2][N3] f32) of its owner
+ *   vr_dspec_a_x2       acc += D22 in
+ *   vr_dspec_a_x1_peer  D11 of this rank's received block, each x1 line's
+ *                       values stored into back[i / L1] ([c][L1][N2][N3] f32)
+ *   vr_dspec_a_final    out = alpha (acc + back) (+ add)
+ * Bit-identical to vr_spec_apply(VR_SPEC_A) on the whole grid.  blk / back
+ * are HOST arrays of nranks device pointers (IPC mappings). */
+int vr_dspec_a_ok(const vr_spec_plan* pl, const vr_spec_plan* px, int nranks);
+int vr_dspec_a_rows(vr_spec_plan* pl, vr_spec_plan* px, const float* in, int ncomp, int nranks, int me,
+                    void* const* blk, void* stream);
+int vr_dspec_a_x2(vr_spec_plan* pl, const float* in, int ncomp, void* stream);
+int vr_dspec_a_x1_peer(vr_spec_plan* pl, vr_spec_plan* px, const float* blk_local, int ncomp, int nranks, int me,
+                       void* const* back, void* stream);
+int vr_dspec_a_final(vr_spec_plan* pl, const float* back_local, int ncomp, double alpha, const float* add,
+                     float* out, void* stream);
+
 /* ---- peer-memory transport (multi-GPU, one process per GPU; dist.py) ---------
  * Symmetric buffers: vr_peer_malloc allocates (zeroed) device memory and
  * returns its CUDA IPC handle (vr_peer_handle_bytes() bytes, host memory);

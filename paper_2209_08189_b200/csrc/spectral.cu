@@ -203,6 +203,16 @@ __device__ __forceinline__ void load_twiddles(double2* tw_s, const double2* __re
   for (int t = threadIdx.x; t < L; t += blockDim.x) tw_s[t] = tw[t];
 }
 
+// ptrs[r] for a per-rank pointer array held in kernel parameters, by a select
+// chain: dynamic indexing would copy the array to local memory (ptxas stack)
+__device__ __forceinline__ void* select_ptr(void* const (&ptrs)[8], int r) {
+  void* d = ptrs[0];
+#pragma unroll
+  for (int q = 1; q < 8; ++q)
+    if (r == q) d = ptrs[q];
+  return d;
+}
+
 // ---- operator symbols (applied between the forward and inverse x1 passes) ----
 struct SpecOp {
   int kind;
@@ -223,7 +233,7 @@ struct SpecOp {
   __device__ __forceinline__ float2* out_at(float2* T, int c, int i, int64_t lstride, int64_t rowoff) const {
     const int p = i / xblk;
     if (pdst[0])
-      return reinterpret_cast<float2*>(pdst[p]) + ((int64_t)(me * ncomp + c) * xblk + (i - p * xblk)) * lstride +
+      return reinterpret_cast<float2*>(select_ptr(pdst, p)) + ((int64_t)(me * ncomp + c) * xblk + (i - p * xblk)) * lstride +
              rowoff;
     return T + xoff(c, i, lstride) + rowoff;
   }
@@ -1115,36 +1125,54 @@ static int d2_r2(int L) { return L == 256 ? 16 : (L == 128 ? 8 : 0); }
 // 5 CTAs / SM at 102 registers 0.837 ms; 256-thread CTAs at 2 / SM 0.757 ms)
 static int g_d2_threads = 128;
 
+// x1 lines of 512 / 1024 / 2048 take the three-step long_kernel
+static int d2_r3(int L) { return L == 512 ? 2 : (L == 1024 ? 4 : (L == 2048 ? 8 : 0)); }
+
 static bool d2_ok(const vr_spec_plan* p) {
   const Dims& d = p->d;
-  const int r1 = d2_r2(d.n1), r2 = d2_r2(d.n2), r3 = d2_r2(d.n3);
+  const int r1 = d2_r2(d.n1) || d2_r3(d.n1), r2 = d2_r2(d.n2), r3 = d2_r2(d.n3);
   return g_a_mode && r1 && r2 && r3 && d.n3 % 64 == 0 && d.n2 % 2 == 0;
 }
 
-template <int R2, int NT>
-static void d2_rows(vr_spec_plan* p, const float* in, float* acc, int ncomp, cudaStream_t s) {
+template <int R2, int NT, bool PEER = false>
+static void d2_rows(vr_spec_plan* p, const float* in, float* acc, int ncomp, cudaStream_t s,
+                    const d2::D2Peer& pe = d2::D2Peer{}) {
   const Dims& d = p->d;
   constexpr size_t sm = d2::smem_bytes<R2, NT>();
-  smem_optin(d2::rows_kernel<R2, NT>, sm);
+  smem_optin(d2::rows_kernel<R2, NT, PEER>, sm);
   const int npairs = d.n1 * d.n2 / 2, lpb = NT / R2;
-  d2::rows_kernel<R2, NT><<<dim3((npairs + lpb - 1) / lpb, ncomp), NT, sm, s>>>(in, acc, npairs, d.n(), p->tw3,
-                                                                                1.0 / d.n3);
+  d2::rows_kernel<R2, NT, PEER><<<dim3((npairs + lpb - 1) / lpb, ncomp), NT, sm, s>>>(in, acc, npairs, d.n(),
+                                                                                      p->tw3, 1.0 / d.n3, pe);
 }
 
-template <int R2, bool FINAL, int NT>
+template <int R2, int MODE, int NT>
 static void d2_strided(vr_spec_plan* p, int axis, const float* in, float* acc, const float* add, float* out,
-                       int ncomp, double alpha, cudaStream_t s) {
+                       int ncomp, double alpha, cudaStream_t s, const d2::D2Peer& pe = d2::D2Peer{}) {
   const Dims& d = p->d;
   constexpr size_t sm = d2::smem_bytes<R2, NT>();
-  smem_optin(d2::strided_kernel<R2, FINAL, NT>, sm);
+  smem_optin(d2::strided_kernel<R2, MODE, NT>, sm);
   const bool ax2 = axis == 2;
   const int L = ax2 ? d.n2 : d.n1;
   const int es = ax2 ? d.n3 : d.n2 * d.n3;
   const int n_outer = ax2 ? d.n1 : d.n2;
   const int outer_stride = ax2 ? d.n2 * d.n3 : d.n3;
   const int nchunks = d.n3 / (2 * (NT / R2));
-  d2::strided_kernel<R2, FINAL, NT><<<dim3(n_outer * nchunks, ncomp), NT, sm, s>>>(
-      in, acc, add, out, d.n3, es, outer_stride, d.n(), ax2 ? p->tw2 : p->tw1, 1.0 / L, alpha);
+  d2::strided_kernel<R2, MODE, NT><<<dim3(n_outer * nchunks, ncomp), NT, sm, s>>>(
+      in, acc, add, out, d.n3, es, outer_stride, d.n(), ax2 ? p->tw2 : p->tw1, 1.0 / L, alpha, pe);
+}
+
+// x1 lines of 512 / 1024 / 2048 (MODE 1: final epilogue, MODE 2: peer store)
+template <int MODE>
+static void d2_long(vr_spec_plan* p, const float* in, const float* acc, const float* add, float* out, int ncomp,
+                    double alpha, cudaStream_t s, const d2::D2Peer& pe = d2::D2Peer{}) {
+  const Dims& d = p->d;
+#define D2LONG(R3, NB)                                                                                         {                                                                                                              constexpr size_t sm = d2::long_smem_bytes<R3, NB>();                                                         smem_optin(d2::long_kernel<R3, NB, MODE>, sm);                                                               d2::long_kernel<R3, NB, MODE><<<dim3(d.n2 * (d.n3 / (2 * NB)), ncomp), NB * 16 * R3, sm, s>>>(                    in, acc, add, out, d.n3, d.n2 * d.n3, d.n3, d.n(), p->tw1, 1.0 / d.n1, alpha, pe);                     }
+  // 256-thread CTAs: the f64 line (16 double2 per thread) needs more than the
+  // 128 registers a 512-thread CTA leaves (spills at R3 = 4 / 8 measured in ptxas)
+  if (d.n1 == 512) D2LONG(2, 8)
+  else if (d.n1 == 1024) D2LONG(4, 4)
+  else D2LONG(8, 2)
+#undef D2LONG
 }
 
 template <int NT>
@@ -1152,10 +1180,11 @@ static void spec_apply_A_d2_nt(vr_spec_plan* p, const float* in, int ncomp, doub
                                float* out, float* acc, cudaStream_t s) {
   const Dims& d = p->d;
   if (d.n3 == 256) d2_rows<16, NT>(p, in, acc, ncomp, s); else d2_rows<8, NT>(p, in, acc, ncomp, s);
-  if (d.n2 == 256) d2_strided<16, false, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
-  else d2_strided<8, false, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
-  if (d.n1 == 256) d2_strided<16, true, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
-  else d2_strided<8, true, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
+  if (d.n2 == 256) d2_strided<16, 0, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  else d2_strided<8, 0, NT>(p, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  if (d.n1 == 256) d2_strided<16, 1, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
+  else if (d.n1 == 128) d2_strided<8, 1, NT>(p, 1, in, acc, add, out, ncomp, alpha, s);
+  else d2_long<1>(p, in, acc, add, out, ncomp, alpha, s);
 }
 
 // out = alpha * (D33 + D22 + D11) in (+ add); the partial sums live in p->T
@@ -1484,6 +1513,86 @@ int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int
   fs::axis256_dist<float2, true><<<dim3(pl->d.n1 * nchunks, ncomp), 256, sm, s>>>(
       reinterpret_cast<const float2*>(recv_inv), pl->T, pe, pl->d.n1, pl->n3h, pl->tw2);
   spec_inverse_z(pl, ncomp, add, out, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// ---- A on x1 slabs through the separable engine ---------------------------------
+// pl: the slab plan {L1, N2, N3}; px: the block plan {N1, L2, N3}, L2 = N2 / P.
+// blk[q] / back[q]: rank q's block buffer [c][N1][L2][N3] and back buffer
+// [c][L1][N2][N3] (f32, symmetric).  The partial sums live in pl's T.
+static bool dsep_ok(const vr_spec_plan* pl, const vr_spec_plan* px, int nranks) {
+  if (!pl || !px || nranks < 1 || nranks > 8 || !g_a_mode) return false;
+  const Dims &a = pl->d, &b = px->d;
+  const int L2 = b.n2;
+  return d2_r2(a.n3) && d2_r2(a.n2) && (d2_r2(b.n1) || d2_r3(b.n1)) && a.n3 % 64 == 0 && b.n3 == a.n3 &&
+         L2 * nranks == a.n2 && L2 % 2 == 0 && a.n1 * nranks == b.n1;
+}
+
+static d2::D2Peer dsep_peer(const vr_spec_plan* pl, const vr_spec_plan* px, int nranks, int me, void* const* dst) {
+  d2::D2Peer pe{};
+  for (int q = 0; q < nranks; ++q) pe.dst[q] = dst[q];
+  pe.me = me;
+  pe.l1 = pl->d.n1;
+  pe.l2 = px->d.n2;
+  pe.n1 = px->d.n1;
+  pe.n2 = pl->d.n2;
+  return pe;
+}
+
+int vr_dspec_a_ok(const vr_spec_plan* pl, const vr_spec_plan* px, int nranks) {
+  return dsep_ok(pl, px, nranks) ? 1 : 0;
+}
+
+// acc = D33 in on the slab; every slab row also goes to blk[j / L2]
+int vr_dspec_a_rows(vr_spec_plan* pl, vr_spec_plan* px, const float* in, int ncomp, int nranks, int me,
+                    void* const* blk, void* stream) {
+  if (!in || !blk || (ncomp != 1 && ncomp != 3) || me < 0 || me >= nranks) return VR_ERR_ARG;
+  if (!dsep_ok(pl, px, nranks)) return VR_ERR_UNSUPPORTED;
+  if (int rc = ensure_scratch(pl, false, true)) return rc;
+  const d2::D2Peer pe = dsep_peer(pl, px, nranks, me, blk);
+  float* acc = reinterpret_cast<float*>(pl->T);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (pl->d.n3 == 256) d2_rows<16, 128, true>(pl, in, acc, ncomp, s, pe);
+  else d2_rows<8, 128, true>(pl, in, acc, ncomp, s, pe);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// acc += D22 in (local x2 lines)
+int vr_dspec_a_x2(vr_spec_plan* pl, const float* in, int ncomp, void* stream) {
+  if (!pl || !in || (ncomp != 1 && ncomp != 3) || !pl->T || !d2_r2(pl->d.n2)) return VR_ERR_ARG;
+  float* acc = reinterpret_cast<float*>(pl->T);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (pl->d.n2 == 256) d2_strided<16, 0, 128>(pl, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  else d2_strided<8, 0, 128>(pl, 2, in, acc, nullptr, nullptr, ncomp, 1.0, s);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// D11 of the received block's x1 lines -> back[i / L1]
+int vr_dspec_a_x1_peer(vr_spec_plan* pl, vr_spec_plan* px, const float* blk_local, int ncomp, int nranks, int me,
+                       void* const* back, void* stream) {
+  if (!blk_local || !back || (ncomp != 1 && ncomp != 3) || me < 0 || me >= nranks) return VR_ERR_ARG;
+  if (!dsep_ok(pl, px, nranks)) return VR_ERR_UNSUPPORTED;
+  const d2::D2Peer pe = dsep_peer(pl, px, nranks, me, back);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n1 = px->d.n1;
+  if (n1 == 256) d2_strided<16, 2, 128>(px, 1, blk_local, nullptr, nullptr, nullptr, ncomp, 1.0, s, pe);
+  else if (n1 == 128) d2_strided<8, 2, 128>(px, 1, blk_local, nullptr, nullptr, nullptr, ncomp, 1.0, s, pe);
+  else d2_long<2>(px, blk_local, nullptr, nullptr, nullptr, ncomp, 1.0, s, pe);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// out = alpha (acc + back) (+ add) on the slab
+int vr_dspec_a_final(vr_spec_plan* pl, const float* back_local, int ncomp, double alpha, const float* add,
+                     float* out, void* stream) {
+  if (!pl || !back_local || !out || (ncomp != 1 && ncomp != 3) || !pl->T) return VR_ERR_ARG;
+  const int64_t n4 = (int64_t)ncomp * pl->d.n() / 4;
+  d2::final_kernel<<<grid_for(n4, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(pl->T), reinterpret_cast<const float4*>(back_local),
+      reinterpret_cast<const float4*>(add), reinterpret_cast<float4*>(out), n4, alpha);
   VR_CHECK_LAUNCH();
   return VR_OK;
 }

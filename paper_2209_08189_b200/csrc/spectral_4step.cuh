@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
     for (int u = 0; u < 16; ++u) {
       const int j = out_freq<R2>(t, u);
       if (INV) out[slab_off(j)] = v[u];
-      else reinterpret_cast<C*>(pe.dst[j >> jshift])[blk_off(pe.me, j & (L2 - 1))] = v[u];
+      else reinterpret_cast<C*>(select_ptr(pe.dst, j >> jshift))[blk_off(pe.me, j & (L2 - 1))] = v[u];
     }
   }
   // (no per-thread system fence: the completion flag is stored by a kernel

@@ -122,6 +122,11 @@ class DistSpectralWorkspace:
         P = ctx.world
         self.peer = (ctx.mesh is not None and not self.generic and n2 == 256 and 1 < P <= 8 and (P & (P - 1)) == 0
                      and os.environ.get("VR_PEER_FUSED", "1") != "0")
+        # A through the separable line engine with the transposes as pass
+        # outputs (csrc/spectral.cu vr_dspec_a_*): f32 rows over NVLink instead
+        # of f64 half spectra, no 3-D transform
+        self.sep_a = (ctx.mesh is not None and 1 < P <= 8 and os.environ.get("VR_DIST_SEP_A", "1") != "0"
+                      and bool(lib.vr_dspec_a_ok(self._pl, self._px, P)))
         self._dst_cache = {}
 
     @property
@@ -201,6 +206,30 @@ class DistSpectralWorkspace:
                                                      st), "vr_dspec_inverse_peer")
         return True
 
+    def _apply_sep_a(self, x, out, add, alpha) -> None:
+        """out = alpha A x (+ add) on the slab: local x3 / x2 line passes, the
+        slab rows stored into the x2-chunk owners' block buffers by the x3
+        pass, the x1 pass on this rank's block storing D11 x back to the slab
+        owners, then alpha (acc + back) (+ add) -- the single-domain
+        operator's arithmetic (spectral_d2.cuh)."""
+        lib, st, ctx = _lib.lib(), _lib.stream(), self.ctx
+        P, me = ctx.world, ctx.rank
+        ncomp = 3 if x.dim() == 4 else 1
+        n = ncomp * (x[0].numel() if ncomp == 3 else x.numel())
+        blk = self.recv.view(torch.float32)[:n]     # [c][N1][L2][N3] -- peers write here
+        back = self.irecv[:n]                       # [c][L1][N2][N3]
+        with _lib.timed("dist.spectral"):
+            _lib.check(lib.vr_dspec_a_rows(self._pl, self._px, x.data_ptr(), ncomp, P, me, self._dst(blk), st),
+                       "vr_dspec_a_rows")
+            e1 = self._signal()
+            _lib.check(lib.vr_dspec_a_x2(self._pl, x.data_ptr(), ncomp, st), "vr_dspec_a_x2")
+            self._wait(e1)
+            _lib.check(lib.vr_dspec_a_x1_peer(self._pl, self._px, blk.data_ptr(), ncomp, P, me, self._dst(back), st),
+                       "vr_dspec_a_x1_peer")
+            self._wait(self._signal())
+            _lib.check(lib.vr_dspec_a_final(self._pl, back.data_ptr(), ncomp, float(alpha), _lib.ptr(add),
+                                            out.data_ptr(), st), "vr_dspec_a_final")
+
     def _exchange(self, dst: torch.Tensor, src: torch.Tensor, ncomp: int, cplx_words: int) -> None:
         """One all-to-all for all components: blocks are [rank][component][...]."""
         m = self.per_comp * cplx_words * ncomp
@@ -216,6 +245,9 @@ class DistSpectralWorkspace:
             out = torch.empty_like(x)
         f64 = kind in (_lib.SPEC_A, _lib.SPEC_A2) or self.generic
         P = self.ctx.world
+        if kind == _lib.SPEC_A and self.sep_a:
+            self._apply_sep_a(x, out, add, alpha)
+            return out
         if self.peer:
             comps = "pipelined" if (ncomp == 3 and kind != _lib.SPEC_K) else "fused"
             if self._apply_peer(kind, x, out, add, f64, beta_v, beta_w, shift, sigma, alpha, comps):

@@ -204,6 +204,12 @@ def case_parity_256(rank, world):
     _dist_vs_single(rank, world, 256, "cubic")
 
 
+def case_parity_weak(rank, world):
+    """The weak-scaling bench shape (256 world, 256, 256): x1 lines of 512 /
+    1024 on the transposed block (separable A's long x1 pass, xdiag_long)."""
+    _dist_vs_single_dims(rank, world, (256 * world, 256, 256), "cubic", 1e-4)
+
+
 @pytest.mark.parametrize("case", ["case_ops_match_single", "case_gn32", "case_c2_64"])
 def test_slab_world1(case):
     spawn(case, 1)
@@ -216,12 +222,12 @@ def test_slab_world2(case):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (gpurun --gpus 2)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak"])
 def test_dist_vs_single_world2(case):
     spawn(case, 2)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs (gpurun --gpus 4)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak"])
 def test_dist_vs_single_world4(case):
     spawn(case, 4)

@@ -85,3 +85,27 @@ def test_inverse_pairs(P):
     back = apply_inv_shifted_A2(P.VectorField(g, lhs), ops, shift).data
     err = float(torch.linalg.vector_norm(back - V.data) / torch.linalg.vector_norm(V.data))
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("dims", [(512, 128, 128), (1024, 128, 256), (2048, 128, 128)])
+def test_separable_A_long_x1(P, dims):
+    """A on the separable line engine with x1 lines of 512 / 1024 / 2048 (the
+    three-step long_kernel; the same kernels run the x1 pass of the distributed
+    A): plane-wave eigenfunctions at 1e-5 and the 3-D f64 engine at 1e-6."""
+    from paper_2209_08189_b200 import _lib
+    g = P.make_grid(dims)
+    ops = P.RegOperators.for_grid(g, 1e-2, 0.0)
+    if dims[0] == 512:
+        f32, f64, ksq = _waves(dims)
+        _check(P.apply_A(P.VectorField(g, f32), ops).data, f64, ksq)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((3,) + dims, device="cuda", generator=gen)
+    sep = P.apply_A(P.VectorField(g, x), ops).data.clone()
+    lib = _lib.lib()
+    prev = lib.vr_set_spec_a_mode(0)
+    try:
+        full = P.apply_A(P.VectorField(g, x), ops).data
+    finally:
+        lib.vr_set_spec_a_mode(prev)
+    err = float(torch.linalg.vector_norm((sep - full).double()) / torch.linalg.vector_norm(full.double()))
+    assert err < 1e-6, err
