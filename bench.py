@@ -287,6 +287,8 @@ def run_ours(args):
     _lib.PROFILE.reset(timed=(dominant, "vr_spec_apply", "vr_trace_rk2", "vr_fd8_grad", "vr_trace_rk2_slab",
                               "vr_dspec_forward", "vr_dspec_xpass", "vr_dspec_inverse", "vr_fd8_grad_slab",
                               "vr_dspec_forward_peer", "vr_dspec_xpass_peer", "vr_dspec_inverse_peer",
+                              "vr_dspec_a_rows", "vr_dspec_a_x2", "vr_dspec_a_x1_peer", "vr_dspec_a_final",
+                              "vr_dspec_a_x2_final",
                               "vr_incstate_step_slab", "vr_incstate_step", "vr_body_force", "dist.ghosts",
                               "dist.alltoall", "dist.allreduce", "dist.sweep", "dist.spectral"))
     clocks = ClockSampler(local)

@@ -298,6 +298,10 @@ int vr_dspec_a_x1_peer(vr_spec_plan* pl, vr_spec_plan* px, const float* blk_loca
                        void* const* back, void* stream);
 int vr_dspec_a_final(vr_spec_plan* pl, const float* back_local, int ncomp, double alpha, const float* add,
                      float* out, void* stream);
+/* vr_dspec_a_x2 and vr_dspec_a_final as one pass, run after the x1 exchange:
+ * out = alpha ((acc + D22 in) + back) (+ add), same roundings. */
+int vr_dspec_a_x2_final(vr_spec_plan* pl, const float* in, const float* back_local, int ncomp, double alpha,
+                        const float* add, float* out, void* stream);
 
 /* ---- peer-memory transport (multi-GPU, one process per GPU; dist.py) ---------
  * Symmetric buffers: vr_peer_malloc allocates (zeroed) device memory and

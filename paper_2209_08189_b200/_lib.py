@@ -88,6 +88,7 @@ _SIGS = {
     "vr_dspec_a_x2": [_p, _p, _i32, _p],
     "vr_dspec_a_x1_peer": [_p, _p, _p, _i32, _i32, _i32, _p, _p],
     "vr_dspec_a_final": [_p, _p, _i32, _f64, _p, _p, _p],
+    "vr_dspec_a_x2_final": [_p, _p, _p, _i32, _f64, _p, _p, _p],
     # peer-memory transport
     "vr_peer_malloc": [_i64, C.POINTER(_p), _p],
     "vr_peer_free": [_p],
@@ -117,7 +118,7 @@ class NativeError(VelregError):
 LAUNCHES = {"vr_spec_apply_launches": 0, "vr_trace_rk2": 2, "vr_h1_energy": 4, "vr_prolong_spectral": 7, "vr_dots": 2, "vr_sqdiff": 2, "vr_label_range": 2,
             "vr_dspec_forward": 3, "vr_dspec_xpass": 1, "vr_dspec_h1_partial": 2, "vr_dspec_inverse": 3,
             "vr_dspec_forward_peer": 2, "vr_dspec_xpass_peer": 1, "vr_dspec_inverse_peer": 2,
-            "vr_dspec_a_ok": 0, "vr_dspec_a_rows": 1, "vr_dspec_a_x2": 1, "vr_dspec_a_x1_peer": 1, "vr_dspec_a_final": 1,
+            "vr_dspec_a_ok": 0, "vr_dspec_a_rows": 1, "vr_dspec_a_x2": 1, "vr_dspec_a_x1_peer": 1, "vr_dspec_a_final": 1, "vr_dspec_a_x2_final": 1,
             "vr_spec_plan_is_fast": 0,
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
             "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0,

@@ -1570,6 +1570,22 @@ int vr_dspec_a_x2(vr_spec_plan* pl, const float* in, int ncomp, void* stream) {
   return VR_OK;
 }
 
+// out = alpha ((acc + D22 in) + back) (+ add): the x2 pass and the final in
+// one kernel (after the x1 exchange), instead of vr_dspec_a_x2 + vr_dspec_a_final
+int vr_dspec_a_x2_final(vr_spec_plan* pl, const float* in, const float* back_local, int ncomp, double alpha,
+                        const float* add, float* out, void* stream) {
+  if (!pl || !in || !back_local || !out || (ncomp != 1 && ncomp != 3) || !pl->T || !d2_r2(pl->d.n2))
+    return VR_ERR_ARG;
+  float* acc = reinterpret_cast<float*>(pl->T);
+  cudaStream_t s = (cudaStream_t)stream;
+  d2::D2Peer pe{};
+  pe.back = back_local;
+  if (pl->d.n2 == 256) d2_strided<16, 3, 128>(pl, 2, in, acc, add, out, ncomp, alpha, s, pe);
+  else d2_strided<8, 3, 128>(pl, 2, in, acc, add, out, ncomp, alpha, s, pe);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
 // D11 of the received block's x1 lines -> back[i / L1]
 int vr_dspec_a_x1_peer(vr_spec_plan* pl, vr_spec_plan* px, const float* blk_local, int ncomp, int nranks, int me,
                        void* const* back, void* stream) {

@@ -48,9 +48,10 @@ namespace d2 {
 // peer destinations of the distributed passes (symmetric buffers, per rank)
 struct D2Peer {
   void* dst[8];
-  int me;       // this rank
-  int l1, l2;   // x1 planes per rank, x2 rows per block
-  int n1, n2;   // global N1, N2
+  const float* back;   // MODE 3: this rank's back buffer (D11 values, slab layout)
+  int me;              // this rank
+  int l1, l2;          // x1 planes per rank, x2 rows per block
+  int n1, n2;          // global N1, N2
 };
 
 // input slot of the forward line FFT for the value thread t holds at output
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) rows_kernel(const float
 // a contiguous 2 NB-float run.  MODE 0: acc += D v; MODE 1 (final):
 // out = alpha (acc + D v) (+ add), acc may alias out (same element, same
 // thread); MODE 2: x1 lines of a distributed block, D v -> the owning rank's
-// back buffer (pe).
+// back buffer (pe); MODE 3: out = alpha ((acc + D v) + back) (+ add).
 template <int R2, int MODE, int NT>
 __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) strided_kernel(const float* __restrict__ v, float* acc,
                                                          const float* __restrict__ add, float* out, int n3, int es,
@@ -199,6 +200,19 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) strided_kernel(const fl
     if (MODE == 1) {
       r.x = final_value(s.x, y[u].x, alpha);
       r.y = final_value(s.y, y[u].y, alpha);
+      if (db) {
+        const float2 b = __ldg(db + e);
+        r.x += b.x;
+        r.y += b.y;
+      }
+      ob[e] = r;
+    } else if (MODE == 3) {
+      // distributed x2 pass after the x1 exchange: the MODE 0 sum, then the
+      // final epilogue with the received D11 values (same roundings as the
+      // single-domain MODE 0 -> MODE 1 sequence)
+      const float2 bk = __ldg(reinterpret_cast<const float2*>(pe.back + cb) + e);
+      r.x = final_value(s.x + y[u].x, bk.x, alpha);
+      r.y = final_value(s.y + y[u].y, bk.y, alpha);
       if (db) {
         const float2 b = __ldg(db + e);
         r.x += b.x;

@@ -89,6 +89,11 @@ class SpectralWorkspace:
         return float(out.cpu()[0])
 
 
+# distributed separable A: x2 pass fused with the final (after the x1
+# exchange, VR_SEP_A_FUSED=1) or overlapping the first exchange (0)
+_SEP_A_FUSED_FINAL = os.environ.get("VR_SEP_A_FUSED", "1") != "0"
+
+
 class DistSpectralWorkspace:
     """Spectral operators on x1 slabs (see csrc/spectral.cu "Distributed"):
     local x3/x2 passes + pack -> one all-to-all per component -> x1 pass with
@@ -218,17 +223,23 @@ class DistSpectralWorkspace:
         n = ncomp * (x[0].numel() if ncomp == 3 else x.numel())
         blk = self.recv.view(torch.float32)[:n]     # [c][N1][L2][N3] -- peers write here
         back = self.irecv[:n]                       # [c][L1][N2][N3]
+        fused = _SEP_A_FUSED_FINAL
         with _lib.timed("dist.spectral"):
             _lib.check(lib.vr_dspec_a_rows(self._pl, self._px, x.data_ptr(), ncomp, P, me, self._dst(blk), st),
                        "vr_dspec_a_rows")
             e1 = self._signal()
-            _lib.check(lib.vr_dspec_a_x2(self._pl, x.data_ptr(), ncomp, st), "vr_dspec_a_x2")
+            if not fused:   # the local x2 pass covers the exchange
+                _lib.check(lib.vr_dspec_a_x2(self._pl, x.data_ptr(), ncomp, st), "vr_dspec_a_x2")
             self._wait(e1)
             _lib.check(lib.vr_dspec_a_x1_peer(self._pl, self._px, blk.data_ptr(), ncomp, P, me, self._dst(back), st),
                        "vr_dspec_a_x1_peer")
             self._wait(self._signal())
-            _lib.check(lib.vr_dspec_a_final(self._pl, back.data_ptr(), ncomp, float(alpha), _lib.ptr(add),
-                                            out.data_ptr(), st), "vr_dspec_a_final")
+            if fused:
+                _lib.check(lib.vr_dspec_a_x2_final(self._pl, x.data_ptr(), back.data_ptr(), ncomp, float(alpha),
+                                                   _lib.ptr(add), out.data_ptr(), st), "vr_dspec_a_x2_final")
+            else:
+                _lib.check(lib.vr_dspec_a_final(self._pl, back.data_ptr(), ncomp, float(alpha), _lib.ptr(add),
+                                                out.data_ptr(), st), "vr_dspec_a_final")
 
     def _exchange(self, dst: torch.Tensor, src: torch.Tensor, ncomp: int, cplx_words: int) -> None:
         """One all-to-all for all components: blocks are [rank][component][...]."""
