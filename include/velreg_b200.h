@@ -318,6 +318,10 @@ int vr_peer_close(void* ptr);
 int vr_peer_handle_bytes(void);
 int vr_peer_copy(void* dst, const void* src, int64_t bytes, void* stream);
 int vr_peer_signal(unsigned long long* flag, unsigned long long value, void* stream);
+/* n <= 8 flags (HOST array of device addresses) in one launch / one batched
+ * stream memory operation (cuStreamBatchMemOp; falls back to n waits). */
+int vr_peer_signal_many(unsigned long long* const* flags, int n, unsigned long long value, void* stream);
+int vr_peer_wait_many(const unsigned long long* const* flags, int n, unsigned long long value, void* stream);
 int vr_peer_wait(const unsigned long long* flag, unsigned long long value, void* stream);
 /* ghost planes of a float slab src (ncomp, L1, N2, N3): planes [0, w) of every
  * component -> left_hi (ncomp, w, N2, N3), planes [L1-w, L1) -> right_lo;

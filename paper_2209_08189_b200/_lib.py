@@ -97,6 +97,8 @@ _SIGS = {
     "vr_peer_handle_bytes": [],
     "vr_peer_copy": [_p, _p, _i64, _p],
     "vr_peer_signal": [_p, C.c_uint64, _p],
+    "vr_peer_signal_many": [_p, _i32, C.c_uint64, _p],
+    "vr_peer_wait_many": [_p, _i32, C.c_uint64, _p],
     "vr_peer_wait": [_p, C.c_uint64, _p],
     "vr_peer_halo_put": [_p, _i32, _i32, _i64, _i32, _p, _p, _p],
 }
@@ -123,7 +125,7 @@ LAUNCHES = {"vr_spec_apply_launches": 0, "vr_trace_rk2": 2, "vr_h1_energy": 4, "
             "vr_minmax": 2, "vr_vecstats": 3, "vr_spec_plan_create": 0, "vr_spec_plan_destroy": 0,
             "vr_spec_plan_dims": 0, "vr_reduce_scratch_doubles": 0,
             "vr_peer_malloc": 0, "vr_peer_free": 0, "vr_peer_open": 0, "vr_peer_close": 0, "vr_peer_handle_bytes": 0,
-            "vr_peer_copy": 0, "vr_peer_wait": 0}
+            "vr_peer_copy": 0, "vr_peer_wait": 0, "vr_peer_wait_many": 0, "vr_peer_signal_many": 1}
 
 
 class Profile:

@@ -30,8 +30,10 @@
 namespace {
 
 typedef CUresult (*PFN_waitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
 PFN_waitValue64 g_wait = nullptr;
+PFN_batchMemOp g_batch = nullptr;
 std::once_flag g_once;
 
 void load_driver_entry_points() {
@@ -41,14 +43,32 @@ void load_driver_entry_points() {
     if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_wait = reinterpret_cast<PFN_waitValue64>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_batch = reinterpret_cast<PFN_batchMemOp>(fn);
   });
 }
+
+constexpr int kMaxFlags = 8;
+struct FlagSet {
+  unsigned long long* f[kMaxFlags];
+  int n;
+};
 
 // one-thread release store of an epoch into a (peer) flag, after a
 // system-scope fence: everything this stream wrote before is visible first
 __global__ void signal_kernel(unsigned long long* flag, unsigned long long value) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+// the same for up to kMaxFlags flags in one launch (one per destination rank)
+__global__ void signal_many_kernel(FlagSet fs, unsigned long long value) {
+  __threadfence_system();
+#pragma unroll
+  for (int i = 0; i < kMaxFlags; ++i)
+    if (i < fs.n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fs.f[i]), "l"(value) : "memory");
 }
 
 // Ghost-plane put: the first w planes of every component go to the left
@@ -139,6 +159,43 @@ int vr_peer_signal(unsigned long long* flag, unsigned long long value, void* str
   signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
   VR_CHECK_LAUNCH();
   return VR_OK;
+}
+
+// flags[0..n) := value in one launch, ordered after all prior work of `stream`
+int vr_peer_signal_many(unsigned long long* const* flags, int n, unsigned long long value, void* stream) {
+  if (!flags || n < 1 || n > kMaxFlags) return VR_ERR_ARG;
+  FlagSet fs{};
+  for (int i = 0; i < n; ++i) {
+    if (!flags[i]) return VR_ERR_ARG;
+    fs.f[i] = flags[i];
+  }
+  fs.n = n;
+  signal_many_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(fs, value);
+  VR_CHECK_LAUNCH();
+  return VR_OK;
+}
+
+// `stream` waits until every *flags[i] >= value: one batched stream memory
+// operation (cuStreamBatchMemOp) instead of n separate waits
+int vr_peer_wait_many(const unsigned long long* const* flags, int n, unsigned long long value, void* stream) {
+  if (!flags || n < 1 || n > kMaxFlags) return VR_ERR_ARG;
+  load_driver_entry_points();
+  if (!g_batch) {
+    for (int i = 0; i < n; ++i)
+      if (int rc = vr_peer_wait(flags[i], value, stream)) return rc;
+    return VR_OK;
+  }
+  CUstreamBatchMemOpParams ops[kMaxFlags];
+  memset(ops, 0, sizeof(ops));
+  for (int i = 0; i < n; ++i) {
+    if (!flags[i]) return VR_ERR_ARG;
+    ops[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+    ops[i].waitValue.address = (CUdeviceptr)flags[i];
+    ops[i].waitValue.value64 = (cuuint64_t)value;
+    ops[i].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  }
+  const CUresult r = g_batch((CUstream)stream, (unsigned)n, ops, 0);
+  return r == CUDA_SUCCESS ? VR_OK : VR_ERR_LAUNCH;
 }
 
 // `stream` waits until *flag >= value (flag in this GPU's memory)

@@ -160,15 +160,12 @@ class DistSpectralWorkspace:
     def _signal(self) -> int:
         mesh, st = self.ctx.mesh, _lib.stream()
         e = mesh._next("a2a")
-        for q in range(self.ctx.world):
-            _lib.check(mesh.lib.vr_peer_signal(mesh._flag_remote(q, self.ctx.rank, mesh.A2A), e, st),
-                       "vr_peer_signal")
+        mesh.signal_many([mesh._flag_remote(q, self.ctx.rank, mesh.A2A) for q in range(self.ctx.world)], e, st)
         return e
 
     def _wait(self, e: int) -> None:
         mesh, st = self.ctx.mesh, _lib.stream()
-        for q in range(self.ctx.world):
-            _lib.check(mesh.lib.vr_peer_wait(mesh._flag_local(q, mesh.A2A), e, st), "vr_peer_wait")
+        mesh.wait_many([mesh._flag_local(q, mesh.A2A) for q in range(self.ctx.world)], e, st)
 
     def _regions(self, c: int, ncomp: int, f64: bool):
         """(recv, irecv) views of component c's regions (or all ncomp from 0)."""

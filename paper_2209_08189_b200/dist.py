@@ -91,8 +91,11 @@ class _PeerWork:
 
     def wait(self) -> None:
         st = _lib.stream()
+        by_epoch = {}
         for addr, e in self.flags:
-            _lib.check(self.mesh.lib.vr_peer_wait(addr, e, st), "vr_peer_wait")
+            by_epoch.setdefault(e, []).append(addr)
+        for e, addrs in by_epoch.items():
+            self.mesh.wait_many(addrs, e, st)
 
 
 class PeerMesh:
@@ -116,6 +119,7 @@ class PeerMesh:
         self.hbytes = int(self.lib.vr_peer_handle_bytes())
         self.side = torch.cuda.Stream()
         self.epoch = {}
+        self._arrays = {}                # flag-address tuples -> ctypes arrays
         self.bufs = {}                   # name -> (local ptr, [ptr on rank q], nbytes)
         self._opened = []
         self.flags, self.flags_remote = self._symmetric(self.P * self.NCH * 8)
@@ -167,6 +171,22 @@ class PeerMesh:
     def _flag_remote(self, q: int, src: int, ch: int) -> int:
         return self.flags_remote[q] + (src * self.NCH + ch) * 8
 
+    def _addr_array(self, addrs):
+        key = tuple(addrs)
+        arr = self._arrays.get(key)
+        if arr is None:
+            arr = (self.C.c_void_p * len(key))(*key)
+            self._arrays[key] = arr
+        return arr
+
+    def signal_many(self, addrs, e: int, st) -> None:
+        """Set the (peer) flags `addrs` to epoch e behind the stream's work: one launch."""
+        _lib.check(self.lib.vr_peer_signal_many(self._addr_array(addrs), len(addrs), e, st), "vr_peer_signal_many")
+
+    def wait_many(self, addrs, e: int, st) -> None:
+        """The stream waits until every local flag in `addrs` reaches epoch e (one batched op)."""
+        _lib.check(self.lib.vr_peer_wait_many(self._addr_array(addrs), len(addrs), e, st), "vr_peer_wait_many")
+
     def _next(self, key: str) -> int:
         e = self.epoch.get(key, 0) + 1
         self.epoch[key] = e
@@ -203,8 +223,8 @@ class PeerMesh:
         st = _lib.stream()
         _lib.check(self.lib.vr_peer_halo_put(xs.data_ptr(), ncomp, L1, n2 * n3, w, remote[left] + off_hi,
                                              remote[right] + off_lo, st), "vr_peer_halo_put")
-        _lib.check(self.lib.vr_peer_signal(self._flag_remote(left, self.me, self.GHOST_HI), e, st), "vr_peer_signal")
-        _lib.check(self.lib.vr_peer_signal(self._flag_remote(right, self.me, self.GHOST_LO), e, st), "vr_peer_signal")
+        self.signal_many((self._flag_remote(left, self.me, self.GHOST_HI),
+                          self._flag_remote(right, self.me, self.GHOST_LO)), e, st)
         shape = lead + (w, n2, n3)
         lo = _view(local + off_lo, blk, x.dtype, shape)
         hi = _view(local + off_hi, blk, x.dtype, shape)
@@ -225,7 +245,7 @@ class PeerMesh:
             q = (self.me + k) % self.P                     # stagger the destinations
             _lib.check(self.lib.vr_peer_copy(self.remote_of(out, q) + self.me * nb, base + q * nb, nb, st),
                        "vr_peer_copy")
-            _lib.check(self.lib.vr_peer_signal(self._flag_remote(q, self.me, self.A2A), e, st), "vr_peer_signal")
+        self.signal_many([self._flag_remote(q, self.me, self.A2A) for q in range(self.P)], e, st)
         return _PeerWork(self, [(self._flag_local(q, self.A2A), e) for q in range(self.P)])
 
 
