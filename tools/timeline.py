@@ -2,6 +2,7 @@
 time vs span, and the largest idle gaps (host-side launch or sync stalls).
 
     python tools/timeline.py [--n 256] [--top 15]
+    torchrun --nproc-per-node N ... tools/timeline.py     # x1 slabs, (256 N, 256, 256); rank 0 reports
 """
 from __future__ import annotations
 
@@ -23,7 +24,16 @@ def main():
     args = ap.parse_args()
     import paper_2209_08189_b200 as P
     from paper_2209_08189_b200.synth import c2_problem
-    g = P.make_grid((args.n,) * 3)
+    from paper_2209_08189_b200 import dist as pdist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    g = P.make_grid((args.n * world, args.n, args.n))
+    act = pdist.activate(pdist.SlabContext(g.dims) if world > 1 else None)
+    act.__enter__()
     m0, m1, _, _, _ = c2_problem(g)
     cfg = P.RegistrationConfig(beta_v=1e-2, beta_w=0.0, n_t=4, interp_order="cubic")
     for _ in range(2):
@@ -33,6 +43,8 @@ def main():
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         P.gauss_newton_register(m0, m1, cfg)
         torch.cuda.synchronize()
+    if rank != 0:
+        return
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0]
     ev.sort(key=lambda e: e.time_range.start)
     t0 = ev[0].time_range.start
