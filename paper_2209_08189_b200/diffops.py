@@ -351,7 +351,8 @@ class DistSpectralWorkspace:
         _lib.check(lib.vr_dspec_h1_partial(self._px, self.recv.data_ptr(), self.ctx.rank * self.ctx.L2,
                                            self.grid.dims[1], self.ctx.L1, TWO_PI ** 3 / (n * n), out.data_ptr(), st),
                    "vr_dspec_h1_partial")
-        return float(self.ctx.allreduce(out.cpu().numpy(), "sum")[0])
+        self.ctx.allreduce_(out, "sum")
+        return float(out.cpu()[0])
 
 
 _ws_cache: dict = {}

@@ -158,9 +158,10 @@ class TransportOperators:
         """Ghost width from the global max |v1| (allreduce), one halo exchange
         of v (covers both the FD8 divergence and the RK2 star points), one of
         div (for the source factors), then the slab trace kernel."""
-        from .reductions import local_absmax, minmax_local
+        from .reductions import minmax
         ctx, cfg = self.ctx, self.cfg
-        vmax1 = float(ctx.allreduce([local_absmax(v[0])], "max")[0])
+        mn, mx, _, _ = minmax(v[0])          # allreduced on the device, one read
+        vmax1 = max(abs(float(mn)), abs(float(mx)))
         w = _dist.ghost_width(vmax1, cfg.dt, self.grid.dims[0], cfg.interp_order)
         ldims = ctx.local_dims
         self.div = fd8_divergence_t(v)
@@ -183,8 +184,8 @@ class TransportOperators:
             # all ranks) and redo the trace with wider ghosts if any departure
             # stencil -- or an interior-plane stencil of the overlapped sweeps --
             # would leave the exchanged planes.
-            mn_f, mx_f, mn_b, mx_b = minmax_local(disp_f[0], disp_b[0])
-            dmax = float(ctx.allreduce([max(abs(mn_f), abs(mx_f), abs(mn_b), abs(mx_b))], "max")[0])
+            mn_f, mx_f, mn_b, mx_b = minmax(disp_f[0], disp_b[0])
+            dmax = float(max(abs(mn_f), abs(mx_f), abs(mn_b), abs(mx_b)))
             if not math.isfinite(dmax):
                 raise TransportError("characteristic trace produced non-finite displacements")
             need = _dist.ghost_width_for_displacement(dmax, cfg.interp_order)
