@@ -204,6 +204,30 @@ def case_parity_256(rank, world):
     _dist_vs_single(rank, world, 256, "cubic")
 
 
+def case_sep_a_bitwise(rank, world):
+    """A on the distributed separable engine (vr_dspec_a_*) equals the
+    single-GPU separable operator bit for bit (same line transforms, same
+    roundings of the partial sums), at 256^3 (block x1 lines of 256) and on
+    the weak-scaling shape (x1 lines of 256 world)."""
+    import paper_2209_08189_b200 as P
+    from paper_2209_08189_b200 import dist, _lib
+    for dims in ((256, 256, 256), (256 * world, 256, 256)):
+        g = P.make_grid(dims)
+        gen = torch.Generator(device="cuda").manual_seed(3)
+        w = torch.randn((3,) + dims, device="cuda", generator=gen)
+        add = torch.randn((3,) + dims, device="cuda", generator=gen)
+        ops = P.RegOperators.for_grid(g, 1e-2, 0.0)
+        ref = ops.workspace.apply(_lib.SPEC_A, w, add=add, alpha=1e-2)
+        ctx = dist.SlabContext(g.dims)
+        sl = slice(ctx.x0, ctx.x0 + ctx.L1)
+        with dist.activate(ctx):
+            ops_s = P.RegOperators.for_grid(g, 1e-2, 0.0)
+            ws = ops_s.workspace
+            assert ws.sep_a, "distributed separable A not selected"
+            got = ws.apply(_lib.SPEC_A, w[:, sl].contiguous(), add=add[:, sl].contiguous(), alpha=1e-2)
+        assert torch.equal(got, ref[:, sl]), (dims, float((got - ref[:, sl]).abs().max()))
+
+
 def case_parity_weak(rank, world):
     """The weak-scaling bench shape (256 world, 256, 256): x1 lines of 512 /
     1024 on the transposed block (separable A's long x1 pass, xdiag_long)."""
@@ -222,12 +246,14 @@ def test_slab_world2(case):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (gpurun --gpus 2)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak",
+                                  "case_sep_a_bitwise"])
 def test_dist_vs_single_world2(case):
     spawn(case, 2)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs (gpurun --gpus 4)")
-@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak"])
+@pytest.mark.parametrize("case", ["case_parity_256", "case_parity_512", "case_parity_clarity", "case_parity_weak",
+                                  "case_sep_a_bitwise"])
 def test_dist_vs_single_world4(case):
     spawn(case, 4)
