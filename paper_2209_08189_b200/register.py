@@ -13,6 +13,7 @@ from dataclasses import dataclass
 
 import torch
 
+from .errors import GridError
 from .grid import Grid, LabelMap, ScalarField, VectorField
 from .metrics import DiceReport, dice_averages
 from .optim import RegistrationConfig, SolverDiagnostics, gauss_newton_solve
@@ -68,11 +69,32 @@ def _upload_async(items, pending: list) -> list:
     return out
 
 
+def _download_async(pairs) -> torch.cuda.Event:
+    """Device -> host copies (pinned destinations) on the side stream, ordered
+    after the current stream's work; returns the completion event."""
+    dev = torch.cuda.current_device()
+    st = _side.get(dev)
+    if st is None:
+        st = _side[dev] = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for host, d in pairs:
+            host.copy_(d, non_blocking=True)
+            d.record_stream(st)
+        ev = torch.cuda.Event()
+        ev.record(st)
+    return ev
+
+
 def register(m0, m1, params: RegistrationConfig | dict | None = None, labels0=None, labels1=None,
-             v0: VectorField | None = None, pre_dice: bool = False, grid: Grid | None = None) -> RegistrationResult:
+             v0: VectorField | None = None, pre_dice: bool = False, grid: Grid | None = None,
+             out_host: tuple | None = None) -> RegistrationResult:
     """Register template m0 to reference m1 (arrays, tensors or ScalarFields;
     pinned host tensors are uploaded asynchronously).  `grid` names the lattice
-    when m0 is a bare array that is only this rank's x1 slab."""
+    when m0 is a bare array that is only this rank's x1 slab.  `out_host` =
+    (velocity, deformed) pinned host tensors: the final velocity and deformed
+    template are copied into them while the labels are transported and scored
+    (complete when this call's stream work is)."""
     if params is None:
         cfg = RegistrationConfig()
     elif isinstance(params, dict):
@@ -81,12 +103,19 @@ def register(m0, m1, params: RegistrationConfig | dict | None = None, labels0=No
         cfg = params
     m0 = _as_field(m0, grid)
     m1 = _as_field(m1, m0.grid)
+    if out_host is not None:
+        shp = tuple(m0.values.shape)
+        if tuple(out_host[0].shape) != (3,) + shp or tuple(out_host[1].shape) != shp:
+            raise GridError("out_host buffers do not match the velocity / deformed template shapes")
     # host label maps (pinned) upload on a side stream while the solver runs
     pending = []
     if labels0 is not None and labels1 is not None:
         labels0, labels1 = _upload_async([labels0, labels1], pending)
     v, diag, state = gauss_newton_solve(m0, m1, cfg, v0)
     res = RegistrationResult(v, state.deformed, diag.relative_residual, diag)
+    copied = None
+    if out_host is not None:
+        copied = _download_async([(out_host[0], v.data), (out_host[1], state.deformed.values)])
     if labels0 is not None and labels1 is not None:
         for ev in pending:
             torch.cuda.current_stream().wait_event(ev)
@@ -96,4 +125,6 @@ def register(m0, m1, params: RegistrationConfig | dict | None = None, labels0=No
         res.dice = dice_averages(moved, l1)
         if pre_dice:
             res.dice_pre = dice_averages(l0, l1)
+    if copied is not None:
+        torch.cuda.current_stream().wait_event(copied)
     return res

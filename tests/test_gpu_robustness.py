@@ -88,3 +88,12 @@ def test_register_from_pinned_host_buffers(P):
     assert got.relative_residual == ref.relative_residual
     assert got.dice.d_a == ref.dice.d_a
     assert torch.equal(got.velocity.data, ref.velocity.data)
+    # results read back into caller-owned pinned buffers during the label scoring
+    hv = torch.empty((3,) + g.dims, dtype=torch.float32).pin_memory()
+    hd = torch.empty(g.dims, dtype=torch.float32).pin_memory()
+    got = P.register(h[0], h[1], cfg, labels0=hl[0], labels1=hl[1], out_host=(hv, hd))
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(hv, ref.velocity.data.cpu()) and torch.equal(hd, ref.deformed.values.cpu())
+    assert got.dice.d_a == ref.dice.d_a
+    with pytest.raises(P.GridError):
+        P.register(h[0], h[1], cfg, out_host=(hd, hv))
