@@ -19,7 +19,7 @@ from . import _lib
 from . import dist as _dist
 from .diffops import fd8_divergence_t, fd8_gradient_t
 from .errors import TransportError
-from .grid import Grid, ScalarField, VectorField, TWO_PI
+from .grid import Grid, ScalarField, VectorField
 
 INTERP_ORDERS = ("linear", "cubic")
 

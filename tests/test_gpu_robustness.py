@@ -3,7 +3,6 @@ the staged sweeps, deferred non-finite flags matched by storage, NaN-aware
 min / max, single-pass label validation, and the slab-context routing."""
 import math
 
-import numpy as np
 import pytest
 import torch
 

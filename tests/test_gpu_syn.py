@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import GOLDEN, golden_json, golden_npz, rel_l2
+from conftest import golden_json, golden_npz, rel_l2
 
 pytestmark = pytest.mark.gpu
 

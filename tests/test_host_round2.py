@@ -2,7 +2,6 @@
 widths from departure displacements, SYN host utilities against the live
 reference, and the volume container's header validation."""
 import math
-import os
 
 import numpy as np
 import pytest

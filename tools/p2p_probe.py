@@ -1,5 +1,5 @@
 """NVLink peer-copy bandwidth between GPU 0 and 1 (single process)."""
-import torch, time
+import torch
 print("can_access_peer", torch.cuda.can_device_access_peer(0, 1), torch.cuda.can_device_access_peer(1, 0))
 for mb in (1, 4, 16, 64, 256):
     a = torch.empty(mb * 2**20 // 4, device="cuda:0")

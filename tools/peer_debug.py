@@ -9,7 +9,7 @@ def main():
     rank = int(os.environ["RANK"]); torch.cuda.set_device(rank)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", rank))
     import paper_2209_08189_b200 as P
-    from paper_2209_08189_b200 import dist, _lib
+    from paper_2209_08189_b200 import dist
     n = int(os.environ.get("N", "256"))
     g = P.make_grid((n, n, n))
     ctx = dist.SlabContext(g.dims)
