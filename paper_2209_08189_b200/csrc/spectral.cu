@@ -845,6 +845,7 @@ static int ensure_scratch(vr_spec_plan* p, bool need_s = true, bool need_t = tru
 // x3 passes of 256-point rows as paired-row four-step kernels (fs::zfwd256_pair /
 // zinv256_pair); vr_set_spectral_tuning(2, 0) selects the Stockham kernels
 static int g_zpair = 1;
+static int g_xflat = 1;   // vr_set_spectral_tuning(4, .): x1 passes (xdiag256 / xdiag_long) over the flat (x2, kz) plane
 static bool zpair_ok(const vr_spec_plan* p) {
   return g_zpair && g_fft_mode && p->fast && p->d.n3 == 256 && (p->d.n1 * p->d.n2) % 2 == 0;
 }
@@ -978,44 +979,45 @@ static int spec_xpass(vr_spec_plan* p, const SpecOp& op, bool reduce, cudaStream
   if (p->fast && g_fft_mode && d.n1 == 256 && !reduce && op.kind != VR_SPEC_K && g_xdiag) {
     // component-diagonal symbol: one component per CTA row, no shared tile
     const int nchunks = (p->n3h + 15) / 16;
-    const dim3 g(d.n2 * nchunks, nc);
-    if (f64) {
-      const size_t sm = sizeof(double2) * 16 * fs::line_smem<16>();
-      smem_optin(fs::xdiag256<double2>, sm);
-      fs::xdiag256<double2><<<g, 256, sm, s>>>(Sd, Tt, d.n2, p->n3h, p->tw1, op);
-    } else {
-      const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
-      smem_optin(fs::xdiag256<float2>, sm);
-      fs::xdiag256<float2><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(Sd), Tt, d.n2, p->n3h, p->tw1, op);
-    }
+    const dim3 g(g_xflat ? (d.n2 * p->n3h + 15) / 16 : d.n2 * nchunks, nc);
+#define XD256(CF, FL)                                                                                         \
+  {                                                                                                          \
+    const size_t sm = sizeof(CF) * 16 * fs::line_smem<16>();                                                 \
+    smem_optin(fs::xdiag256<CF, FL>, sm);                                                                    \
+    fs::xdiag256<CF, FL><<<g, 256, sm, s>>>(reinterpret_cast<const CF*>(Sd), Tt, d.n2, p->n3h, p->tw1, op); \
+  }
+    if (f64 && g_xflat) XD256(double2, true)
+    else if (f64) XD256(double2, false)
+    else if (g_xflat) XD256(float2, true)
+    else XD256(float2, false)
+#undef XD256
     return g.x;
   }
   if (p->fast && g_fft_mode && g_xdiag && !reduce && op.kind != VR_SPEC_K &&
       (d.n1 == 512 || d.n1 == 1024 || d.n1 == 2048)) {
     // long x1 lines (the transposed block of a 2 / 4 / 8-rank x1-slab run):
     // three-step register FFT, one component per grid row
+#define XLONG_LAUNCH(CF, R3, NB, FL)                                                                          \
+  {                                                                                                          \
+    const int nblk = FL ? (d.n2 * p->n3h + NB - 1) / NB : d.n2 * ((p->n3h + NB - 1) / NB);                   \
+    const size_t sm = sizeof(CF) * NB * fs::lf3::smem_elems<R3>();                                           \
+    smem_optin(fs::xdiag_long<CF, R3, NB, FL>, sm);                                                          \
+    fs::xdiag_long<CF, R3, NB, FL><<<dim3(nblk, nc), NB * 16 * R3, sm, s>>>(                                 \
+        reinterpret_cast<const CF*>(Sd), Tt, d.n2, p->n3h, p->tw1, op);                                      \
+    return nblk;                                                                                             \
+  }
 #define XLONG(R3, NBF, NBD)                                                                                  \
   {                                                                                                          \
-    if (f64) {                                                                                               \
-      const int nch = (p->n3h + NBD - 1) / NBD;                                                              \
-      const size_t sm = sizeof(double2) * NBD * fs::lf3::smem_elems<R3>();                                   \
-      smem_optin(fs::xdiag_long<double2, R3, NBD>, sm);                                                      \
-      fs::xdiag_long<double2, R3, NBD><<<dim3(d.n2 * nch, nc), NBD * 16 * R3, sm, s>>>(Sd, Tt, d.n2, p->n3h,  \
-                                                                                       p->tw1, op);          \
-      return d.n2 * nch;                                                                                     \
-    } else {                                                                                                 \
-      const int nch = (p->n3h + NBF - 1) / NBF;                                                              \
-      const size_t sm = sizeof(float2) * NBF * fs::lf3::smem_elems<R3>();                                   \
-      smem_optin(fs::xdiag_long<float2, R3, NBF>, sm);                                                       \
-      fs::xdiag_long<float2, R3, NBF><<<dim3(d.n2 * nch, nc), NBF * 16 * R3, sm, s>>>(                       \
-          reinterpret_cast<const float2*>(Sd), Tt, d.n2, p->n3h, p->tw1, op);                                \
-      return d.n2 * nch;                                                                                     \
-    }                                                                                                        \
+    if (f64 && g_xflat) XLONG_LAUNCH(double2, R3, NBD, true)                                                 \
+    else if (f64) XLONG_LAUNCH(double2, R3, NBD, false)                                                      \
+    else if (g_xflat) XLONG_LAUNCH(float2, R3, NBF, true)                                                    \
+    else XLONG_LAUNCH(float2, R3, NBF, false)                                                                \
   }
     if (d.n1 == 512) XLONG(2, 16, 8)
     if (d.n1 == 1024) XLONG(4, 8, 8)
     XLONG(8, 4, 4)
 #undef XLONG
+#undef XLONG_LAUNCH
   }
   if (p->fast && g_fft_mode && g_xdiag && !reduce && op.kind == VR_SPEC_K && nc == 3 && !f64 &&
       (d.n1 == 512 || d.n1 == 1024 || d.n1 == 2048)) {
@@ -1215,6 +1217,12 @@ int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp) {
 int vr_set_spectral_tuning(int key, int value) {
   // key 1: per-component scheduling of diagonal symbols (1 = on, 0 = all components per pass)
   // key 2: paired-row four-step x3 passes for 256-point rows (1 = on, 0 = Stockham)
+  // key 4: x1 pass (xdiag256) over the flat (x2, kz) plane (1) or 16 kz of one x2 row per CTA (0)
+  if (key == 4) {
+    const int prev = g_xflat;
+    g_xflat = value;
+    return prev;
+  }
   if (key == 2) {
     const int prev = g_zpair;
     g_zpair = value;

@@ -237,19 +237,33 @@ __device__ __forceinline__ void diag_symbol_at(const SpecOp& op, int k1, double 
   v = vals[0];
 }
 
-template <typename CF>
+// FLAT: the CTA's NB lines are NB consecutive positions p = j n3h + kz of the
+// (x2, kz) plane instead of NB kz of one x2 row -- every line load is one
+// aligned 128-byte segment and no CTA idles on the odd n3h = n3 / 2 + 1
+// (with 16 kz per row, 129 columns take 9 chunks, the last holding one).
+template <typename CF, bool FLAT = false>
 __global__ void __launch_bounds__(256, sizeof(CF) == 8 ? VR_F32_CTAS : 2) xdiag256(const CF* __restrict__ S,
                                                                       float2* __restrict__ T, int n2, int n3h,
                                                                       const double2* __restrict__ tw, SpecOp op) {
   constexpr int R2 = 16, NB = 16, L = 256;
   extern __shared__ __align__(16) unsigned char fs_smem[];
   const int q = threadIdx.x % NB, t = threadIdx.x / NB;
-  const int nchunks = (n3h + NB - 1) / NB;
-  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB;
+  int j, kz;
+  bool ok;
+  if (FLAT) {
+    const int p = blockIdx.x * NB + q;
+    ok = p < n2 * n3h;
+    j = p / n3h;
+    kz = p - j * n3h;
+  } else {
+    const int nchunks = (n3h + NB - 1) / NB;
+    j = blockIdx.x / nchunks;
+    kz = (blockIdx.x - j * nchunks) * NB + q;
+    ok = kz < n3h;
+  }
   const int c = blockIdx.y;
-  const bool ok = kz0 + q < n3h;
   const int64_t lstride = (int64_t)n2 * n3h;
-  const CF* sb = S + (int64_t)j * n3h + kz0 + q;
+  const CF* sb = S + (int64_t)j * n3h + kz;
   CF v[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(256, sizeof(CF) == 8 ? VR_F32_CTAS : 2) xdiag2
   }
   CF* sm = reinterpret_cast<CF*>(fs_smem) + q * line_smem<R2>();
   line_fft<CF, R2>(v, t, sm, tw, false);
-  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)(kz0 + q);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)kz;
   float2 w[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
@@ -269,7 +283,7 @@ __global__ void __launch_bounds__(256, sizeof(CF) == 8 ? VR_F32_CTAS : 2) xdiag2
   __syncthreads();   // transpose scratch reused by the inverse
   line_fft<float2, R2>(w, t, reinterpret_cast<float2*>(fs_smem) + q * line_smem<R2>(), tw, true);
   if (ok) {
-    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
+    const int64_t rowoff = (int64_t)j * n3h + kz;
 #pragma unroll
     for (int u = 0; u < 16; ++u) *op.out_at(T, c, out_freq<R2>(t, u), lstride, rowoff) = w[u];
   }
@@ -457,19 +471,30 @@ __device__ __forceinline__ void inverse(C (&v)[16], int u, C* sm, const double2*
 // X pass for component-diagonal symbols on long lines (L = 256 R3): NB
 // consecutive kz per CTA (lane = q + NB u), one component per grid row;
 // forward in CF, symbol, inverse in f32 -> T (or the peer destinations).
-template <typename CF, int R3, int NB>
+// FLAT: lines over the flat (x2, kz) plane, as xdiag256<., true>
+template <typename CF, int R3, int NB, bool FLAT = false>
 __global__ void __launch_bounds__(NB * 16 * R3, 1) xdiag_long(const CF* __restrict__ S, float2* __restrict__ T,
                                                               int n2, int n3h, const double2* __restrict__ twL,
                                                               SpecOp op) {
   constexpr int Tn = lf3::T<R3>(), L = 256 * R3, LS = lf3::smem_elems<R3>();
   extern __shared__ __align__(16) unsigned char fs_smem[];
   const int q = threadIdx.x % NB, u = threadIdx.x / NB;
-  const int nchunks = (n3h + NB - 1) / NB;
-  const int j = blockIdx.x / nchunks, kz0 = (blockIdx.x - j * nchunks) * NB;
+  int j, kz;
+  bool ok;
+  if (FLAT) {
+    const int p = blockIdx.x * NB + q;
+    ok = p < n2 * n3h;
+    j = p / n3h;
+    kz = p - j * n3h;
+  } else {
+    const int nchunks = (n3h + NB - 1) / NB;
+    j = blockIdx.x / nchunks;
+    kz = (blockIdx.x - j * nchunks) * NB + q;
+    ok = kz < n3h;
+  }
   const int c = blockIdx.y;
-  const bool ok = kz0 + q < n3h;
   const int64_t lstride = (int64_t)n2 * n3h;
-  const CF* sb = S + (int64_t)j * n3h + kz0 + q;
+  const CF* sb = S + (int64_t)j * n3h + kz;
   CF v[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -477,7 +502,7 @@ __global__ void __launch_bounds__(NB * 16 * R3, 1) xdiag_long(const CF* __restri
     else { v[m].x = 0; v[m].y = 0; }
   }
   lf3::forward<CF, R3>(v, u, reinterpret_cast<CF*>(fs_smem) + q * LS, twL);
-  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)(kz0 + q);
+  const double k2 = (double)signed_freq(j + op.j0, op.n2g), k3 = (double)kz;
   float2 w[16];
 #pragma unroll
   for (int idx = 0; idx < 16; ++idx) {
@@ -488,7 +513,7 @@ __global__ void __launch_bounds__(NB * 16 * R3, 1) xdiag_long(const CF* __restri
   __syncthreads();   // the shared buffer is reused by the f32 inverse
   lf3::inverse<float2, R3>(w, u, reinterpret_cast<float2*>(fs_smem) + q * LS, twL);
   if (ok) {
-    const int64_t rowoff = (int64_t)j * n3h + kz0 + q;
+    const int64_t rowoff = (int64_t)j * n3h + kz;
 #pragma unroll
     for (int m = 0; m < 16; ++m) *op.out_at(T, c, u + Tn * m, lstride, rowoff) = w[m];
   }
