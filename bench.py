@@ -315,7 +315,7 @@ def run_ours(args):
     value = t_step   # seconds per registration of the whole job (max over ranks)
 
     # ---- e2e through the public API from pinned host buffers -------------------
-    e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
     h_m0 = torch.from_numpy(m0.numpy()).pin_memory()
     h_m1 = torch.from_numpy(m1.numpy()).pin_memory()
     h_l0 = torch.from_numpy(l0.numpy()).pin_memory()
