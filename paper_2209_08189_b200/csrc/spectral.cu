@@ -525,9 +525,6 @@ static int g_fft_mode = 1;
 // A = |k|^2 through the separable f64 line engine (spectral_d2.cuh) where the
 // line lengths allow; vr_set_spec_a_mode(0) selects the 3-D f64 path.
 static int g_a_mode = 1;
-// vr_set_spectral_tuning(4, .): strided 256-point passes (axis256, axis256_dist)
-// and the x1 passes (xdiag256 / xdiag_long) over the flat (outer, kz) index space
-static int g_xflat = 1;
 // x1 pass of component-diagonal symbols without the 3-component shared tile
 // (fs::xdiag256); vr_set_fft_mode(2) turns it off for A/B checks.
 static bool g_xdiag = true;
@@ -802,17 +799,15 @@ static void launch_axis(vr_spec_plan* p, C* buf, int axis, int ncomp, int inv, c
     const int nchunks = (p->n3h + 15) / 16;
     const size_t sm = sizeof(C) * 16 * fs::line_smem<16>();
     const double2* twL = ax2 ? p->tw2 : p->tw1;
-    const dim3 g(g_xflat ? (n_outer * p->n3h + 15) / 16 : n_outer * nchunks, ncomp);
-#define AX256(INV, FL)                                                                                        \
-  {                                                                                                          \
-    smem_optin(fs::axis256<C, INV, FL>, sm);                                                                 \
-    fs::axis256<C, INV, FL><<<g, 256, sm, s>>>(buf, es, n_outer, outer_stride, p->nspec, p->n3h, twL);       \
-  }
-    if (inv && g_xflat) AX256(true, true)
-    else if (inv) AX256(true, false)
-    else if (g_xflat) AX256(false, true)
-    else AX256(false, false)
-#undef AX256
+    if (inv) {
+      smem_optin(fs::axis256<C, true>, sm);
+      fs::axis256<C, true><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, es, n_outer, outer_stride, p->nspec,
+                                                                          p->n3h, twL);
+    } else {
+      smem_optin(fs::axis256<C, false>, sm);
+      fs::axis256<C, false><<<dim3(n_outer * nchunks, ncomp), 256, sm, s>>>(buf, es, n_outer, outer_stride, p->nspec,
+                                                                           p->n3h, twL);
+    }
     return;
   }
   if (p->fast) {
@@ -850,6 +845,7 @@ static int ensure_scratch(vr_spec_plan* p, bool need_s = true, bool need_t = tru
 // x3 passes of 256-point rows as paired-row four-step kernels (fs::zfwd256_pair /
 // zinv256_pair); vr_set_spectral_tuning(2, 0) selects the Stockham kernels
 static int g_zpair = 1;
+static int g_xflat = 1;   // vr_set_spectral_tuning(4, .): x1 passes (xdiag256 / xdiag_long) over the flat (x2, kz) plane
 static bool zpair_ok(const vr_spec_plan* p) {
   return g_zpair && g_fft_mode && p->fast && p->d.n3 == 256 && (p->d.n1 * p->d.n2) % 2 == 0;
 }
@@ -1221,7 +1217,7 @@ int vr_spec_apply_launches(const vr_spec_plan* p, int kind, int ncomp) {
 int vr_set_spectral_tuning(int key, int value) {
   // key 1: per-component scheduling of diagonal symbols (1 = on, 0 = all components per pass)
   // key 2: paired-row four-step x3 passes for 256-point rows (1 = on, 0 = Stockham)
-  // key 4: 256-point strided / x1 passes over the flat (outer, kz) index space (1) or 16 kz of one row per CTA (0)
+  // key 4: x1 pass (xdiag256) over the flat (x2, kz) plane (1) or 16 kz of one x2 row per CTA (0)
   if (key == 4) {
     const int prev = g_xflat;
     g_xflat = value;
@@ -1476,19 +1472,17 @@ int vr_dspec_forward_peer(vr_spec_plan* pl, const float* in, int ncomp, int f64,
   pe.l2shift = log2i(nranks);
   pe.ncomp = ncomp;
   const int nchunks = (pl->n3h + 15) / 16;
-  const dim3 g(g_xflat ? (pl->d.n1 * pl->n3h + 15) / 16 : pl->d.n1 * nchunks, ncomp);
-#define AXD(CF, FL)                                                                                           \
-  {                                                                                                          \
-    const size_t sm = sizeof(CF) * 16 * fs::line_smem<16>();                                                 \
-    smem_optin(fs::axis256_dist<CF, false, FL>, sm);                                                         \
-    fs::axis256_dist<CF, false, FL><<<g, 256, sm, s>>>(reinterpret_cast<const CF*>(pl->S), nullptr, pe,      \
-                                                       pl->d.n1, pl->n3h, pl->tw2);                          \
+  const dim3 g(pl->d.n1 * nchunks, ncomp);
+  if (f64) {
+    const size_t sm = sizeof(double2) * 16 * fs::line_smem<16>();
+    smem_optin(fs::axis256_dist<double2, false>, sm);
+    fs::axis256_dist<double2, false><<<g, 256, sm, s>>>(pl->S, nullptr, pe, pl->d.n1, pl->n3h, pl->tw2);
+  } else {
+    const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
+    smem_optin(fs::axis256_dist<float2, false>, sm);
+    fs::axis256_dist<float2, false><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(pl->S), nullptr, pe,
+                                                       pl->d.n1, pl->n3h, pl->tw2);
   }
-  if (f64 && g_xflat) AXD(double2, true)
-  else if (f64) AXD(double2, false)
-  else if (g_xflat) AXD(float2, true)
-  else AXD(float2, false)
-#undef AXD
   VR_CHECK_LAUNCH();
   return VR_OK;
 }
@@ -1523,16 +1517,9 @@ int vr_dspec_inverse_peer(vr_spec_plan* pl, const void* recv_inv, int ncomp, int
   pe.ncomp = ncomp;
   const int nchunks = (pl->n3h + 15) / 16;
   const size_t sm = sizeof(float2) * 16 * fs::line_smem<16>();
-  const dim3 g(g_xflat ? (pl->d.n1 * pl->n3h + 15) / 16 : pl->d.n1 * nchunks, ncomp);
-  if (g_xflat) {
-    smem_optin(fs::axis256_dist<float2, true, true>, sm);
-    fs::axis256_dist<float2, true, true><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(recv_inv), pl->T, pe,
-                                                            pl->d.n1, pl->n3h, pl->tw2);
-  } else {
-    smem_optin(fs::axis256_dist<float2, true>, sm);
-    fs::axis256_dist<float2, true><<<g, 256, sm, s>>>(reinterpret_cast<const float2*>(recv_inv), pl->T, pe,
-                                                      pl->d.n1, pl->n3h, pl->tw2);
-  }
+  smem_optin(fs::axis256_dist<float2, true>, sm);
+  fs::axis256_dist<float2, true><<<dim3(pl->d.n1 * nchunks, ncomp), 256, sm, s>>>(
+      reinterpret_cast<const float2*>(recv_inv), pl->T, pe, pl->d.n1, pl->n3h, pl->tw2);
   spec_inverse_z(pl, ncomp, add, out, s);
   VR_CHECK_LAUNCH();
   return VR_OK;

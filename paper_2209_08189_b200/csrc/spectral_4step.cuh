@@ -137,30 +137,17 @@ __device__ __forceinline__ int out_freq(int t, int u) {
 
 // ---- strided axis pass (x2 or plain x1), L = 256: NB lines (consecutive kz) per CTA,
 // 16 threads per line, lane = line + NB * t.  grid (n_outer * nchunks, ncomp)
-// FLAT: the NB lines are NB consecutive positions o n3h + kz of the flat
-// (outer, kz) index space (a chunk may straddle two outer rows) instead of NB
-// kz of one outer row -- no CTA idles on the odd n3h (grid n_outer n3h / NB).
-template <typename C, bool INV, bool FLAT = false>
+template <typename C, bool INV>
 __global__ void __launch_bounds__(256, sizeof(C) == 8 ? VR_F32_CTAS : 2) axis256(C* __restrict__ S, int64_t es, int n_outer, int64_t outer_stride,
                                                int64_t comp_stride, int n3h, const double2* __restrict__ tw) {
   constexpr int R2 = 16, NB = 16;
   extern __shared__ __align__(16) unsigned char fs_smem[];
   C* smem = reinterpret_cast<C*>(fs_smem);
   const int q = threadIdx.x % NB, t = threadIdx.x / NB;
-  int o, kz;
-  bool ok;
-  if (FLAT) {
-    const int p = blockIdx.x * NB + q;
-    ok = p < n_outer * n3h;
-    o = p / n3h;
-    kz = p - o * n3h;
-  } else {
-    const int nchunks = (n3h + NB - 1) / NB;
-    o = blockIdx.x / nchunks;
-    kz = (blockIdx.x - o * nchunks) * NB + q;
-    ok = kz < n3h;
-  }
-  C* base = S + blockIdx.y * comp_stride + o * outer_stride + kz;
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int o = blockIdx.x / nchunks, kz0 = (blockIdx.x - o * nchunks) * NB;
+  const bool ok = kz0 + q < n3h;
+  C* base = S + blockIdx.y * comp_stride + o * outer_stride + kz0 + q;
   C v[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -317,7 +304,7 @@ struct X2Peer {
   int me, l2shift, ncomp;
 };
 
-template <typename C, bool INV, bool FLAT = false>
+template <typename C, bool INV>
 __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(const C* __restrict__ in,
                                                                           C* __restrict__ out, X2Peer pe, int L1,
                                                                           int n3h, const double2* __restrict__ tw) {
@@ -325,24 +312,13 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) axis256_dist(cons
   extern __shared__ __align__(16) unsigned char fs_smem[];
   C* smem = reinterpret_cast<C*>(fs_smem);
   const int q = threadIdx.x % NB, t = threadIdx.x / NB;
-  const int c = blockIdx.y;
-  int i, kz;
-  bool ok;
-  if (FLAT) {   // as axis256<., ., true>: lines over the flat (i, kz) index space
-    const int p = blockIdx.x * NB + q;
-    ok = p < L1 * n3h;
-    i = p / n3h;
-    kz = p - i * n3h;
-  } else {
-    const int nchunks = (n3h + NB - 1) / NB;
-    i = blockIdx.x / nchunks;
-    kz = (blockIdx.x - i * nchunks) * NB + q;
-    ok = kz < n3h;
-  }
+  const int nchunks = (n3h + NB - 1) / NB;
+  const int i = blockIdx.x / nchunks, kz0 = (blockIdx.x - i * nchunks) * NB, c = blockIdx.y;
+  const bool ok = kz0 + q < n3h;
   const int L2 = N2 >> pe.l2shift, jshift = 8 - pe.l2shift;   // row j -> (r, jl) = (j >> jshift, j & (L2-1))
-  auto slab_off = [&](int j) -> int64_t { return (((int64_t)c * L1 + i) * N2 + j) * n3h + kz; };
+  auto slab_off = [&](int j) -> int64_t { return (((int64_t)c * L1 + i) * N2 + j) * n3h + kz0 + q; };
   auto blk_off = [&](int r, int jl) -> int64_t {
-    return ((((int64_t)r * pe.ncomp + c) * L1 + i) * L2 + jl) * n3h + kz;
+    return ((((int64_t)r * pe.ncomp + c) * L1 + i) * L2 + jl) * n3h + kz0 + q;
   };
   C v[16];
 #pragma unroll
