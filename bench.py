@@ -10,9 +10,9 @@ the velocity/deformed-image read-back (e2e).  Synthetic data.
 
 N > 1 (default, "weak"): every GPU keeps a 256^3 block of one registration on
 the x1-extended lattice (256*N, 256, 256) -- the same C2 generator -- decomposed
-into x1 slabs (dist.py: NCCL halo exchange for the SL / FD8 stencils, one
-all-to-all per spectral transpose, allreduce of the PCG/GN scalars),
-max-over-ranks device time.  --strong decomposes the fixed N=1 problem instead.
+into x1 slabs (dist.py: ghost planes and spectral transposes over peer memory
+-- CUDA IPC buffers written by the producing kernels over NVLink, epoch flags --
+NCCL allreduce of the PCG/GN scalars), max-over-ranks device time.  --strong decomposes the fixed N=1 problem instead.
 --n / --order / --nt / --beta-w select other sizes, e.g. the C3 shape
 `--n 1024 --order linear --nt 16 --beta-w 1e-4` (cubic lattice, strong).
 
@@ -404,7 +404,7 @@ def run_ours(args):
             "config": {"workload": f"C2 sphere->deformed sphere {'x'.join(map(str, g.dims))} GN-PCG, {args.order}, "
                                    f"n_t={args.nt}, beta_v=1e-2, beta_w={args.beta_w:g}, gtol=5e-2"
                                    + (f" (weak scaling: 256^3 per GPU)" if weak else ""),
-                       "parallelism": f"x1-slab x{ws} (NCCL halo / all-to-all / allreduce)" if ws > 1 else "single",
+                       "parallelism": f"x1-slab x{ws} (peer-memory halo / transposes, NCCL allreduce)" if ws > 1 else "single",
                        "l2": "256 MB buffer written between timed steps; working set > 126 MB L2",
                        "gn_iterations": diag.gn_iterations,
                        "pcg": [r.pcg_iterations for r in diag.iterations],
