@@ -13,8 +13,9 @@ the x1-extended lattice (256*N, 256, 256) -- the same C2 generator -- decomposed
 into x1 slabs (dist.py: ghost planes and spectral transposes over peer memory
 -- CUDA IPC buffers written by the producing kernels over NVLink, epoch flags --
 NCCL allreduce of the PCG/GN scalars), max-over-ranks device time.  --strong decomposes the fixed N=1 problem instead.
---n / --order / --nt / --beta-w select other sizes, e.g. the C3 shape
-`--n 1024 --order linear --nt 16 --beta-w 1e-4` (cubic lattice, strong).
+--grid / --order / --nt / --beta-w select other sizes, e.g. the C3 shape
+`--grid 1024 --order linear --nt 16 --beta-w 1e-4` (cubic lattice, strong; under
+torchrun spell it --grid: torchrun reads an abbreviated --n as its own option).
 
 --impl reference: ONE full C2 256^3 registration through the live reference
 package (velreg, installed into oracle/_ref by oracle/build_ref.sh; numpy +
