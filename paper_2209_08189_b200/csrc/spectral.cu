@@ -1164,34 +1164,16 @@ static void d2_strided(vr_spec_plan* p, int axis, const float* in, float* acc, c
 }
 
 // x1 lines of 512 / 1024 / 2048 (MODE 1: final epilogue, MODE 2: peer store)
-static int g_long_pipe = 1;   // vr_set_spectral_tuning(5, .): persistent pipelined long_kernel
-
 template <int MODE>
 static void d2_long(vr_spec_plan* p, const float* in, const float* acc, const float* add, float* out, int ncomp,
                     double alpha, cudaStream_t s, const d2::D2Peer& pe = d2::D2Peer{}) {
   const Dims& d = p->d;
-#define D2LONG(R3, NB)                                                                                   \
-  if (g_long_pipe) {                                                                                     \
-    constexpr size_t sm = d2::long_pipe_smem_bytes<R3, NB>();                                            \
-    smem_optin(d2::long_pipe_kernel<R3, NB, MODE>, sm);                                                  \
-    const int ntiles = d.n2 * (d.n3 / (2 * NB)) * ncomp;                                                 \
-    d2::long_pipe_kernel<R3, NB, MODE><<<std::min(ntiles, 148), NB * 16 * R3, sm, s>>>(                  \
-        in, acc, add, out, d.n3, d.n2 * d.n3, d.n3, d.n2, ncomp, d.n(), p->tw1, 1.0 / d.n1, alpha, pe);  \
-  } else {                                                                                               \
-    constexpr size_t sm = d2::long_smem_bytes<R3, NB>();                                                 \
-    smem_optin(d2::long_kernel<R3, NB, MODE>, sm);                                                       \
-    d2::long_kernel<R3, NB, MODE><<<dim3(d.n2 * (d.n3 / (2 * NB)), ncomp), NB * 16 * R3, sm, s>>>(       \
-        in, acc, add, out, d.n3, d.n2 * d.n3, d.n3, d.n(), p->tw1, 1.0 / d.n1, alpha, pe);               \
-  }
+#define D2LONG(R3, NB)                                                                                         {                                                                                                              constexpr size_t sm = d2::long_smem_bytes<R3, NB>();                                                         smem_optin(d2::long_kernel<R3, NB, MODE>, sm);                                                               d2::long_kernel<R3, NB, MODE><<<dim3(d.n2 * (d.n3 / (2 * NB)), ncomp), NB * 16 * R3, sm, s>>>(                    in, acc, add, out, d.n3, d.n2 * d.n3, d.n3, d.n(), p->tw1, 1.0 / d.n1, alpha, pe);                     }
   // 256-thread CTAs: the f64 line (16 double2 per thread) needs more than the
   // 128 registers a 512-thread CTA leaves (spills at R3 = 4 / 8 measured in ptxas)
-  if (d.n1 == 512) {
-    D2LONG(2, 8)
-  } else if (d.n1 == 1024) {
-    D2LONG(4, 4)
-  } else {
-    D2LONG(8, 2)
-  }
+  if (d.n1 == 512) D2LONG(2, 8)
+  else if (d.n1 == 1024) D2LONG(4, 4)
+  else D2LONG(8, 2)
 #undef D2LONG
 }
 
@@ -1236,12 +1218,6 @@ int vr_set_spectral_tuning(int key, int value) {
   // key 1: per-component scheduling of diagonal symbols (1 = on, 0 = all components per pass)
   // key 2: paired-row four-step x3 passes for 256-point rows (1 = on, 0 = Stockham)
   // key 4: x1 pass (xdiag256) over the flat (x2, kz) plane (1) or 16 kz of one x2 row per CTA (0)
-  // key 5: separable engine's long x1 lines as a persistent cp.async-pipelined kernel (1) or one tile per CTA (0)
-  if (key == 5) {
-    const int prev = g_long_pipe;
-    g_long_pipe = value;
-    return prev;
-  }
   if (key == 4) {
     const int prev = g_xflat;
     g_xflat = value;

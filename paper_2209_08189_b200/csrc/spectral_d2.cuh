@@ -234,16 +234,27 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 4) strided_kernel(const fl
 template <int R3, int NB> constexpr size_t long_smem_bytes() {
   return sizeof(double2) * NB * fs::lf3::smem_elems<R3>();
 }
-// transform + epilogue of one tile (NB complex lines = 2 NB columns from k0 of
-// outer row o, component c); x holds the thread's 16 line values x[u + Tn m]
 template <int R3, int NB, int MODE>
-__device__ __forceinline__ void long_finish(double2 (&x)[16], int q, int u, int c, int o, int k0,
-                                            const float* acc, const float* __restrict__ add, float* out, int n3,
-                                            int es, int outer_stride, int64_t cstride,
-                                            const double2* __restrict__ twL, double scale, double alpha,
-                                            const D2Peer& pe, unsigned char* sm) {
+__global__ void __launch_bounds__(NB * 16 * R3, 1) long_kernel(const float* __restrict__ v, const float* acc,
+                                                               const float* __restrict__ add, float* out, int n3,
+                                                               int es, int outer_stride, int64_t cstride,
+                                                               const double2* __restrict__ twL, double scale,
+                                                               double alpha, D2Peer pe) {
   constexpr int Tn = fs::lf3::T<R3>(), L = 256 * R3, LS = fs::lf3::smem_elems<R3>();
-  fs::lf3::forward<double2, R3>(x, u, reinterpret_cast<double2*>(sm) + q * LS, twL);
+  extern __shared__ __align__(16) unsigned char d2_smem[];
+  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
+  const int nchunks = n3 / (2 * NB);
+  const int o = blockIdx.x / nchunks, k0 = (blockIdx.x - o * nchunks) * 2 * NB;
+  const int64_t cb = blockIdx.y * cstride;
+  const int64_t base = (int64_t)o * outer_stride + k0 + 2 * q;
+  const float2* vb = reinterpret_cast<const float2*>(v + cb);
+  double2 x[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const float2 a = __ldg(vb + ((base + (int64_t)(u + Tn * m) * es) >> 1));
+    x[m] = make_double2(a.x, a.y);
+  }
+  fs::lf3::forward<double2, R3>(x, u, reinterpret_cast<double2*>(d2_smem) + q * LS, twL);
   float2 y[16];
 #pragma unroll
   for (int idx = 0; idx < 16; ++idx) {
@@ -253,13 +264,11 @@ __device__ __forceinline__ void long_finish(double2 (&x)[16], int q, int u, int 
     y[idx] = make_float2((float)(x[idx].x * m), (float)(x[idx].y * m));
   }
   __syncthreads();   // the shared buffer is reused by the f32 inverse
-  fs::lf3::inverse<float2, R3>(y, u, reinterpret_cast<float2*>(sm) + q * LS, twL);
+  fs::lf3::inverse<float2, R3>(y, u, reinterpret_cast<float2*>(d2_smem) + q * LS, twL);
   if constexpr (MODE == 2) {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) store_back(pe, c, u + Tn * m, o, k0 + 2 * q, n3, y[m]);
+    for (int m = 0; m < 16; ++m) store_back(pe, blockIdx.y, u + Tn * m, o, k0 + 2 * q, n3, y[m]);
   } else {
-    const int64_t cb = c * cstride;
-    const int64_t base = (int64_t)o * outer_stride + k0 + 2 * q;
     const float2* ab = reinterpret_cast<const float2*>(acc + cb);
     float2* ob = reinterpret_cast<float2*>(out + cb);
     const float2* db = add ? reinterpret_cast<const float2*>(add + cb) : nullptr;
@@ -276,86 +285,6 @@ __device__ __forceinline__ void long_finish(double2 (&x)[16], int q, int u, int 
       ob[e] = r;
     }
   }
-}
-
-template <int R3, int NB, int MODE>
-__global__ void __launch_bounds__(NB * 16 * R3, 1) long_kernel(const float* __restrict__ v, const float* acc,
-                                                               const float* __restrict__ add, float* out, int n3,
-                                                               int es, int outer_stride, int64_t cstride,
-                                                               const double2* __restrict__ twL, double scale,
-                                                               double alpha, D2Peer pe) {
-  constexpr int Tn = fs::lf3::T<R3>();
-  extern __shared__ __align__(16) unsigned char d2_smem[];
-  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
-  const int nchunks = n3 / (2 * NB);
-  const int o = blockIdx.x / nchunks, k0 = (blockIdx.x - o * nchunks) * 2 * NB;
-  const int64_t base = (int64_t)o * outer_stride + k0 + 2 * q;
-  const float2* vb = reinterpret_cast<const float2*>(v + blockIdx.y * cstride);
-  double2 x[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    const float2 a = __ldg(vb + ((base + (int64_t)(u + Tn * m) * es) >> 1));
-    x[m] = make_double2(a.x, a.y);
-  }
-  long_finish<R3, NB, MODE>(x, q, u, blockIdx.y, o, k0, acc, add, out, n3, es, outer_stride, cstride, twL, scale,
-                            alpha, pe, d2_smem);
-}
-
-// Persistent, software-pipelined long_kernel (one CTA per SM -- the f64 line
-// needs ~240 registers, so residency is one CTA either way): the next tile's
-// input block (L rows x 2 NB floats) is prefetched by 16-byte cp.async into a
-// double buffer while the current tile is transformed.
-template <int R3, int NB> constexpr size_t long_pipe_smem_bytes() {
-  return sizeof(double2) * NB * fs::lf3::smem_elems<R3>() + 2 * sizeof(float) * 256 * R3 * 2 * NB;
-}
-template <int R3, int NB, int MODE>
-__global__ void __launch_bounds__(NB * 16 * R3, 1) long_pipe_kernel(const float* __restrict__ v, const float* acc,
-                                                                    const float* __restrict__ add, float* out,
-                                                                    int n3, int es, int outer_stride, int n_outer,
-                                                                    int ncomp, int64_t cstride,
-                                                                    const double2* __restrict__ twL, double scale,
-                                                                    double alpha, D2Peer pe) {
-  constexpr int Tn = fs::lf3::T<R3>(), L = 256 * R3, COLS = 2 * NB, Q = COLS / 4, NTH = NB * 16 * R3;
-  extern __shared__ __align__(16) unsigned char d2_smem[];
-  float* vbuf = reinterpret_cast<float*>(d2_smem + sizeof(double2) * NB * fs::lf3::smem_elems<R3>());
-  const int q = threadIdx.x % NB, u = threadIdx.x / NB;
-  const int nchunks = n3 / COLS;
-  const int per_comp = n_outer * nchunks;
-  const int ntiles = per_comp * ncomp;
-  auto issue = [&](int tile, int buf) {
-    const int c = tile / per_comp, r = tile - c * per_comp;
-    const int o = r / nchunks, k0 = (r - o * nchunks) * COLS;
-    const float* src = v + c * cstride + (int64_t)o * outer_stride + k0;
-    float* dst = vbuf + buf * L * COLS;
-    for (int e = threadIdx.x; e < L * Q; e += NTH) {
-      const int row = e / Q, part = e - row * Q;
-      const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(dst + row * COLS + part * 4));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(src + (int64_t)row * es + part * 4)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  int tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, 0);
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, (it + 1) & 1);
-    else asm volatile("cp.async.commit_group;\n" ::: "memory");   // one group per step
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();
-    const int c = tile / per_comp, r = tile - c * per_comp;
-    const int o = r / nchunks, k0 = (r - o * nchunks) * COLS;
-    const float* vb = vbuf + (it & 1) * L * COLS + 2 * q;
-    double2 x[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const float2 a = *reinterpret_cast<const float2*>(vb + (u + Tn * m) * COLS);
-      x[m] = make_double2(a.x, a.y);
-    }
-    long_finish<R3, NB, MODE>(x, q, u, c, o, k0, acc, add, out, n3, es, outer_stride, cstride, twL, scale, alpha,
-                              pe, d2_smem);
-    __syncthreads();   // vbuf[it & 1] and the line scratch are rewritten next step
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // distributed final: out = alpha (acc + back) (+ add), n4 float4s
