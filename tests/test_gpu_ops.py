@@ -82,6 +82,26 @@ def test_fd8_bit_exact_sizes(P, dims):
     np.testing.assert_array_equal(_np(P.fd8_divergence(P.VectorField(g, w)).values), O.div(w))
 
 
+@pytest.mark.parametrize("dims", [(64, 64, 64), (16, 24, 256)])
+def test_fd8_bit_exact_tiny_band(P, dims):
+    """Sums between 2^-124 and 2^-100 (far-field values of transported
+    templates) take the inline scaled reciprocal path: still IEEE bits, in both
+    the tile and the row-tile kernels."""
+    from oracle import velreg_oracle as O
+    from paper_2209_08189_b200 import _lib
+    rng = np.random.default_rng(11)
+    g = P.make_grid(dims)
+    f = (rng.standard_normal(dims) * 10.0 ** rng.uniform(-37, -29, size=dims)).astype(np.float32)
+    ref = O.grad(f)
+    lib = _lib.lib()
+    for mode in (0, 1):
+        prev = lib.vr_set_fd8_mode(mode)
+        try:
+            np.testing.assert_array_equal(_np(P.fd8_gradient(P.ScalarField(g, f)).data), ref)
+        finally:
+            lib.vr_set_fd8_mode(prev)
+
+
 @pytest.mark.parametrize("dims", [(32, 40, 128), (20, 32, 256)])
 def test_fd8_row_kernel_matches_tile_kernel(P, dims):
     """vr_set_fd8_mode A/B: the bulk-copy row-tile kernel and the cp.async tile
