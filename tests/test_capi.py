@@ -50,3 +50,24 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", src).split('"""')[-1] or "import oracle" not in src, f
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_new_entries_reject_bad_arguments_without_touching_the_gpu():
+    """Host-side argument checks of the round-2 entries return the documented
+    codes before any launch (callable on a machine without a GPU)."""
+    import ctypes as C
+    from paper_2209_08189_b200 import _lib
+    lib = _lib.load_library()
+    ERR_ARG = -1
+    assert lib.vr_dspec_a_ok(None, None, 2) == 0
+    assert lib.vr_dspec_a_rows(None, None, None, 3, 2, 0, None, None) in (ERR_ARG, -5)
+    assert lib.vr_dspec_a_x1_peer(None, None, None, 3, 2, 0, None, None) in (ERR_ARG, -5)
+    assert lib.vr_dspec_a_x2(None, None, 3, None) == ERR_ARG
+    assert lib.vr_dspec_a_final(None, None, 3, 1.0, None, None, None) == ERR_ARG
+    assert lib.vr_dspec_a_x2_final(None, None, None, 3, 1.0, None, None, None) == ERR_ARG
+    flags = (C.c_void_p * 9)(*([None] * 9))
+    assert lib.vr_peer_signal_many(None, 1, 1, None) == ERR_ARG
+    assert lib.vr_peer_signal_many(flags, 9, 1, None) == ERR_ARG      # more than 8 destinations
+    assert lib.vr_peer_signal_many(flags, 1, 1, None) == ERR_ARG      # null flag address
+    assert lib.vr_peer_wait_many(None, 1, 1, None) == ERR_ARG
+    assert lib.vr_peer_wait_many(flags, 0, 1, None) == ERR_ARG
